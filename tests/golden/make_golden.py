@@ -1,0 +1,258 @@
+"""Generate golden vectors by running the UNMODIFIED reference package.
+
+Run in the build container (the reference is not on the GPU box):
+
+    python tests/golden/make_golden.py [case ...]
+
+For every case in ``cases.py`` this drives the reference's public API
+(``prompt_head_data``/``recovery_ratio``/``profile_model``/``encode_prompt``/
+``generate_step``) through a duck-typed array model over the
+seeded workload tensors.  The planted head bias is folded exactly into
+two extra Q/K dimensions (q'=[q*sqrt(d')/sqrt(d), 1, 1],
+k'=[k, slope*j*sqrt(d'), sink*sqrt(d')*[special]]), because the reference
+has no logit-bias hook; under the causal softmax -slope*|i-j| equals
++slope*j up to a row constant.  Decode is teacher-forced with the
+workload's own token ids.  Outputs are written to ``tests/golden/*.npz``.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+REF_SRC = "/root/reference/pkg/src"
+REF_TESTS = "/root/reference/pkg/tests"
+sys.path.insert(0, REF_SRC)
+
+import cases as C  # noqa: E402
+from adaptive_kv import (  # noqa: E402
+    ProfilerConfig, RowAveraging, SelectionCriterion, encode_prompt,
+    feasible_set, generate_step, parse_policy, profile_model, recovery_ratio,
+    retained_indices,
+)
+from adaptive_kv.engine import prompt_head_data  # noqa: E402
+from adaptive_kv.model import ModelConfig, SyntheticModel  # noqa: E402
+from adaptive_kv.policies import PolicyAtom, cache_memory_cost  # noqa: E402
+from adaptive_kv.profiler import masked_cosine_similarity  # noqa: E402
+from adaptive_kv.tokens import TokenClass, VocabMetadata  # noqa: E402
+
+from paper_2310_01801_b200.workloads import PUNCT_IDS, SPECIAL_IDS, VOCAB_SIZE  # noqa: E402
+
+ATOM_BITS = {PolicyAtom.SPECIAL: 1, PolicyAtom.PUNCTUATION: 2, PolicyAtom.FREQUENT: 4,
+             PolicyAtom.LOCAL: 8, PolicyAtom.FULL: 16}
+NAME_ATOM = {"special": PolicyAtom.SPECIAL, "punct": PolicyAtom.PUNCTUATION,
+             "frequent": PolicyAtom.FREQUENT, "local": PolicyAtom.LOCAL}
+
+
+def atom_bits(policy) -> int:
+    return sum(ATOM_BITS[a] for a in policy.atoms)
+
+
+class ArrayModel:
+    """Duck-typed reference model (model.py:150-286 protocol) over arrays
+    q,k,v [G, T, d] (float64) of one token sequence, with the planted bias
+    folded into two extra dimensions."""
+
+    def __init__(self, q, k, v, slopes, sinks, vocab):
+        self.q, self.k, self.v = q, k, v
+        self.slopes, self.sinks = slopes, sinks
+        g, _, d = q.shape
+        self.d = d
+        self.d2 = d + 2
+        self.config = ModelConfig(num_layers=1, num_heads=g, head_dim=d + 2,
+                                  vocab_size=1, seed=0)
+        self.vocab = vocab
+        self._qscale = math.sqrt(self.d2) / math.sqrt(d)
+
+    def k_row(self, layer, head, pos, klass, prompt_len):
+        row = np.zeros(self.d2)
+        row[: self.d] = self.k[head, pos]
+        row[self.d] = self.slopes[head] * pos * math.sqrt(self.d2)
+        row[self.d + 1] = self.sinks[head] * math.sqrt(self.d2) * (klass is TokenClass.SPECIAL)
+        return row
+
+    def q_row(self, layer, head, pos, prompt_len):
+        row = np.ones(self.d2)
+        row[: self.d] = self.q[head, pos] * self._qscale
+        return row
+
+    def v_row(self, layer, head, pos):
+        return self.v[head, pos].copy()
+
+    def head_logits(self, concat):
+        return np.zeros(1)
+
+
+def profiler_cfg(w, opts, T):
+    order = [NAME_ATOM[a] for a in opts.get("order", C.ORDER_DEFAULT)]
+    drop = [NAME_ATOM[a] for a in opts.get("drop", ())]
+    fam = feasible_set(r_l=w.r_l, r_f=w.r_f, atom_order=order, drop=drop)
+    return ProfilerConfig(
+        recovery_threshold=T, feasible=fam,
+        criterion=SelectionCriterion(opts.get("criterion", "recovery")),
+        rows=RowAveraging(opts.get("rows", "all")))
+
+
+def run_sequence(model, tokens, N, D, cfg_list, decode_cfg, fixed):
+    """Reference run for one token sequence: per-head profiling tables for
+    every threshold in cfg_list, then a teacher-forced decode session."""
+    grid = model.config.head_grid()
+    _, _, head_data = prompt_head_data(model, list(tokens[:N]))
+    fam = cfg_list[0].feasible if fixed is None else (fixed,)
+    rows = cfg_list[0].rows
+    R = np.zeros((len(grid), len(fam)))
+    cost = np.zeros((len(grid), len(fam)), dtype=np.int64)
+    cos = np.zeros((len(grid), len(fam)))
+    colsum = np.zeros((len(grid), N))
+    lastrow = np.zeros((len(grid), N))
+    for gi, key in enumerate(grid):
+        A, ctx = head_data[key]
+        colsum[gi] = ctx.cumulative_scores
+        lastrow[gi] = A.matrix[N - 1]
+        for fi, pol in enumerate(fam):
+            ret = retained_indices(pol, ctx)
+            R[gi, fi] = recovery_ratio(A, ret, rows)
+            cost[gi, fi] = cache_memory_cost(pol, ctx)
+            cos[gi, fi] = masked_cosine_similarity(A, ret)
+    csvs, choice = [], np.zeros((len(grid), len(cfg_list)), dtype=np.int64)
+    if fixed is None:
+        for ti, cfg in enumerate(cfg_list):
+            prof = profile_model(head_data, cfg, grid=grid)
+            csvs.append(prof.to_csv())
+            for gi, key in enumerate(grid):
+                choice[gi, ti] = list(cfg.feasible).index(prof[key].policy)
+
+    # decode session (engine.py:203-371), teacher-forced
+    if fixed is None:
+        prof, cache = encode_prompt(model, list(tokens[:N]), decode_cfg, diagnostics=True)
+    else:
+        prof, cache = encode_prompt(model, list(tokens[:N]), None, fixed_policy=fixed,
+                                    diagnostics=True)
+        csvs.append(prof.to_csv())
+    total = N + D
+    enc_kept = np.zeros((len(grid), N), dtype=bool)
+    enc_out = np.zeros((len(grid), model.v.shape[-1]))
+    enc_rec = np.zeros(len(grid))
+    dec_choice = np.zeros(len(grid), dtype=np.int64)
+    for gi, key in enumerate(grid):
+        st = cache.heads[key]
+        enc_kept[gi, st.positions] = True
+        enc_out[gi] = st.pending_output
+        enc_rec[gi] = prof[key].recovery
+        dec_choice[gi] = list(fam).index(st.policy)
+    generate_step(model, cache, None)
+    dec_kept = np.zeros((D, len(grid), total), dtype=bool)
+    dec_out = np.zeros((D, len(grid), model.v.shape[-1]))
+    for t in range(D):
+        generate_step(model, cache, int(tokens[N + t]))
+        rec = cache.last_record.retained_positions
+        for gi, key in enumerate(grid):
+            dec_kept[t, gi, list(rec[key])] = True
+            dec_out[t, gi] = cache.heads[key].pending_output
+    return dict(R=R, cost=cost, cos=cos, colsum=colsum, lastrow=lastrow, choice=choice,
+                csvs=csvs, enc_kept=enc_kept, enc_out=enc_out, enc_rec=enc_rec,
+                dec_choice=dec_choice, dec_kept=dec_kept, dec_out=dec_out,
+                family=np.array([atom_bits(p) for p in fam]))
+
+
+def make_workload_case(name):
+    w, opts = C.case_workload(name)
+    heads = C.case_heads(w, opts)
+    vocab = VocabMetadata(special_ids=frozenset(SPECIAL_IDS), punctuation_ids=frozenset(PUNCT_IDS))
+    fixed = parse_policy(opts["fixed"]) if "fixed" in opts else None
+    cfg_list = [profiler_cfg(w, opts, T) for T in w.thresholds]
+    decode_cfg = profiler_cfg(w, opts, opts.get("decode_T", w.thresholds[0]))
+    per_b = {}
+    for b, h in heads:
+        per_b.setdefault(b, []).append(h)
+    parts, tokens = [], {}
+    for b, hs in sorted(per_b.items()):
+        tok = w.tokens(b)
+        tokens[b] = tok
+        qs, ks, vs = zip(*(w.head_qkv(b, h) for h in hs))
+        model = ArrayModel(np.stack(qs).astype(np.float64), np.stack(ks).astype(np.float64),
+                           np.stack(vs).astype(np.float64), w.slopes[hs], w.sinks[hs], vocab)
+        parts.append(run_sequence(model, tok, w.N, w.D, cfg_list, decode_cfg, fixed))
+    out = {}
+    for key in ("R", "cost", "cos", "colsum", "lastrow", "choice", "enc_kept", "enc_out",
+                "enc_rec", "dec_choice"):
+        out[key] = np.concatenate([p[key] for p in parts], axis=0)
+    out["dec_kept"] = np.packbits(np.concatenate([p["dec_kept"] for p in parts], axis=1), axis=-1)
+    out["enc_kept"] = np.packbits(out["enc_kept"], axis=-1)
+    out["dec_out"] = np.concatenate([p["dec_out"] for p in parts], axis=1)
+    out["family"] = parts[0]["family"]
+    # CSV per threshold, one block per batch row (the reference grid is per sequence)
+    out["csvs"] = np.array(["\n---\n".join(p["csvs"][i] for p in parts)
+                            for i in range(len(parts[0]["csvs"]))])
+    out["heads"] = np.array(heads, dtype=np.int64)
+    out["tokens"] = np.stack([tokens[b] for b in sorted(tokens)])
+    np.savez_compressed(C.golden_path(name), **out)
+
+
+def make_mixed():
+    sys.path.insert(0, REF_TESTS)
+    from conftest import MIXED_PLAN_4X4  # the reference's own fixture
+
+    m = C.MIXED
+    cfgm = ModelConfig(num_layers=4, num_heads=4, head_dim=16, vocab_size=48, seed=m["seed"])
+    model = SyntheticModel(cfgm, MIXED_PLAN_4X4, dominance=m["dominance"])
+    P, S = m["prompt_len"], m["steps"]
+    prompt = model.prompt_token_ids(P)
+    cfg = ProfilerConfig(recovery_threshold=m["T"])
+    prof, cache = encode_prompt(model, prompt, cfg, diagnostics=True)
+    grid = sorted(cfgm.head_grid())
+    enc_kept = np.zeros((len(grid), P), dtype=bool)
+    enc_out = np.zeros((len(grid), 16))
+    for gi, key in enumerate(grid):
+        enc_kept[gi, cache.heads[key].positions] = True
+        enc_out[gi] = cache.heads[key].pending_output
+    tok, _ = generate_step(model, cache, None)
+    tokens = list(prompt)
+    dec_kept = np.zeros((S, len(grid), P + S), dtype=bool)
+    dec_out = np.zeros((S, len(grid), 16))
+    for t in range(S):
+        tokens.append(tok)
+        tok, _ = generate_step(model, cache, tokens[-1])
+        rec = cache.last_record.retained_positions
+        for gi, key in enumerate(grid):
+            dec_kept[t, gi, list(rec[key])] = True
+            dec_out[t, gi] = cache.heads[key].pending_output
+    T = len(tokens)
+    klass = [model.vocab.classify_id(t) for t in tokens]
+    q = np.zeros((len(grid), T, 16))
+    k = np.zeros((len(grid), T, 16))
+    v = np.zeros((len(grid), T, 16))
+    for gi, (l, h) in enumerate(grid):
+        for p in range(T):
+            q[gi, p] = model.q_row(l, h, p, P)
+            k[gi, p] = model.k_row(l, h, p, klass[p], P)
+            v[gi, p] = model.v_row(l, h, p)
+    choice = np.array([list(cfg.feasible).index(prof[key].policy) for key in grid])
+    np.savez_compressed(
+        C.golden_path(m["name"]), q=q, k=k, v=v, tokens=np.array(tokens),
+        special=np.array(sorted(model.vocab.special_ids)),
+        punct=np.array(sorted(model.vocab.punctuation_ids)),
+        choice=choice, csv=np.array(prof.to_csv()),
+        enc_kept=np.packbits(enc_kept, axis=-1), enc_out=enc_out,
+        dec_kept=np.packbits(dec_kept, axis=-1), dec_out=dec_out)
+
+
+def main(argv):
+    names = argv or list(C.CASES) + [C.MIXED["name"]]
+    for name in names:
+        t0 = time.time()
+        if name == C.MIXED["name"]:
+            make_mixed()
+        else:
+            make_workload_case(name)
+        print(f"{name}: {time.time() - t0:.1f}s", flush=True)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])
