@@ -1,0 +1,192 @@
+/*
+ * akv.h — C ABI of libakv_sm100a.so, the B200 (sm_100a) implementation of
+ * FastGen's adaptive-KV hot path: prompt profiling (K1), per-head KV
+ * compaction (K2) and compressed decode with fused insert/evict (K3).
+ *
+ * The reference (arxiv/paper_2310_01801, /root/reference/pkg/src/adaptive_kv)
+ * is a pure-Python/numpy package with no FFI; each entry point below replaces
+ * the per-head numpy loops of one reference function and is bound from the
+ * Python host layer with ctypes:
+ *
+ *   akv_profile      <- engine.py:161-200  prompt_head_data (causal_attention,
+ *                                          A.sum(axis=0)),
+ *                       profiler.py:70-87  recovery_ratio,
+ *                       profiler.py:135-145 select_policy,
+ *                       profiler.py:148-178 select_policy_by_similarity,
+ *                       policies.py:244-267 retained_indices (candidates=None),
+ *                       engine.py:248,255  pending_output = A[n-1] @ V
+ *   akv_compact      <- engine.py:236-259  encode_prompt compaction loop,
+ *                       policies.py:270-288 apply_policy
+ *   akv_decode_step  <- engine.py:303-350  generate_step per-head body,
+ *                       engine.py:93-97    _attend_row,
+ *                       policies.py:332-360 update_cumulative_scores,
+ *                       policies.py:244-267 retained_indices (candidates=live)
+ *
+ * Conventions: plain pointers and sizes only.  All pointers named *_dev are
+ * device pointers; calls are stream-ordered with no implicit host sync and
+ * are reentrant across streams (each call's scratch lives in the caller's
+ * workspace).  The caller owns all memory.  Heads are flattened
+ * g = b*H + h.  Status codes are returned; akv_last_error() gives a
+ * thread-local message.
+ */
+#ifndef AKV_H
+#define AKV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define AKV_OK 0
+#define AKV_ERR_INVALID 1     /* invalid argument (maps to PolicyError/ProfilerError/EngineError) */
+#define AKV_ERR_CAPACITY 2    /* cache segment capacity exceeded / workspace too small */
+#define AKV_ERR_UNSUPPORTED 3 /* unsupported shape or dtype */
+#define AKV_ERR_CUDA 4        /* CUDA runtime error */
+
+/* element types of Q/K/V and of the compressed cache */
+#define AKV_DTYPE_F32 0
+#define AKV_DTYPE_BF16 1
+
+/* policy atoms (policies.py:29-34) as bit flags; FULL excludes the others */
+#define AKV_ATOM_SPECIAL 1
+#define AKV_ATOM_PUNCT 2
+#define AKV_ATOM_FREQUENT 4
+#define AKV_ATOM_LOCAL 8
+#define AKV_ATOM_FULL 16
+
+/* token classes (tokens.py:15-18) */
+#define AKV_CLS_OTHER 0
+#define AKV_CLS_SPECIAL 1
+#define AKV_CLS_PUNCT 2
+
+/* profiler.py:41-48 */
+#define AKV_ROWS_ALL 0
+#define AKV_ROWS_LAST 1
+#define AKV_CRIT_RECOVERY 0
+#define AKV_CRIT_COSINE 1
+
+#define AKV_MAX_FAMILY 8
+#define AKV_MAX_THRESHOLDS 8
+
+/* ---- K1: prompt profiling ------------------------------------------- */
+typedef struct akv_profile_args {
+  int32_t B, H, N, d;            /* batch rows, heads, prompt length, head dim (16,32,64,128) */
+  int32_t dtype;                 /* AKV_DTYPE_* of q/k/v */
+  const void* q_dev;             /* [B,H,ld,d]; rows 0..N-1 of each head are the prompt */
+  const void* k_dev;
+  const void* v_dev;
+  int64_t ld;                    /* rows per head in q/k/v (>= N) */
+  const uint8_t* cls_dev;        /* [B,cls_ld] class of every position */
+  int64_t cls_ld;
+  const float* slope_dev;        /* [H] planted -slope*|i-j| bias, or NULL */
+  const float* sink_dev;         /* [H] planted +sink on special keys, or NULL */
+  int32_t n_family;              /* feasible family (policies.py:304-329), last usually FULL */
+  uint8_t family_atoms[AKV_MAX_FAMILY];
+  double family_r_l[AKV_MAX_FAMILY];
+  double family_r_f[AKV_MAX_FAMILY];
+  int32_t n_thresholds;          /* thresholds[0] drives keep_mask/kept_pos */
+  double thresholds[AKV_MAX_THRESHOLDS];
+  int32_t rows;                  /* AKV_ROWS_* */
+  int32_t criterion;             /* AKV_CRIT_* */
+  /* outputs (device, all [B*H,...]) */
+  float* lse_dev;                /* [B*H,N] row log-sum-exp */
+  double* colsum_dev;            /* [B*H,N] attention mass per key (frequency signal) */
+  double* colsq_dev;             /* [B*H,N] sum of squared weights per key (cosine) */
+  float* lastp_dev;              /* [B*H,N] A[N-1,:] */
+  float* out_last_dev;           /* [B*H,d] A[N-1,:] @ V (pending output) */
+  double* recovery_dev;          /* [B*H,n_family] */
+  int32_t* cost_dev;             /* [B*H,n_family] retained tokens */
+  double* cosine_dev;            /* [B*H,n_family] */
+  int8_t* choice_dev;            /* [B*H,n_thresholds] family index, -1 if none met T */
+  int32_t* kept_pos_dev;         /* [B*H,N] ascending kept positions of the chosen policy */
+  int32_t* kept_count_dev;       /* [B*H] */
+  double* last_row_recovery_dev; /* [B*H] A[N-1, kept].sum() */
+  double* topk_gap_dev;          /* [B*H] min relative score gap at any frequent boundary */
+  void* workspace_dev;
+  size_t workspace_bytes;
+} akv_profile_args;
+
+size_t akv_profile_workspace_size(int32_t B, int32_t H, int32_t N, int32_t d);
+int akv_profile(const akv_profile_args* a, void* stream);
+
+/* ---- K2: compaction into the ragged head-major cache ----------------- */
+typedef struct akv_compact_args {
+  int32_t B, H, N, d;
+  int32_t dtype;
+  const void* k_dev;             /* [B,H,ld,d] */
+  const void* v_dev;
+  int64_t ld;
+  const uint8_t* cls_dev;        /* [B,cls_ld] */
+  int64_t cls_ld;
+  const int32_t* kept_pos_dev;   /* [B*H,N] from akv_profile */
+  const int32_t* kept_count_dev; /* [B*H] */
+  const double* colsum_dev;      /* [B*H,N] scores copied for FREQUENT heads */
+  const uint8_t* head_atoms_dev; /* [B*H] atoms of each head's chosen policy */
+  const int64_t* seg_off_dev;    /* [B*H] first slot of each head's segment */
+  const int32_t* seg_cap_dev;    /* [B*H] segment capacity (slots) */
+  void* kc_dev;                  /* [total_slots,d] compressed K (dtype) */
+  void* vc_dev;                  /* [total_slots,d] compressed V */
+  int32_t* meta_dev;             /* [total_slots] position | class << 24 */
+  double* score_dev;             /* [total_slots] cumulative score (FREQUENT heads) */
+  int32_t* live_dev;             /* [B*H] out: live slots */
+} akv_compact_args;
+
+int akv_compact(const akv_compact_args* a, void* stream);
+/* Device prefix sum of capacities: seg_cap[g] = round_up(kept_count[g] + extra, 8),
+ * seg_off = exclusive scan; *total_dev = sum (int64).  Lets the host size the
+ * arena with a single 8-byte device->host read. */
+int akv_plan_segments(int32_t G, const int32_t* kept_count_dev, int32_t extra,
+                      int32_t* seg_cap_dev, int64_t* seg_off_dev, int64_t* total_dev,
+                      void* stream);
+
+/* ---- K3: one decode step over the compressed cache ------------------- */
+typedef struct akv_decode_args {
+  int32_t B, H, d;
+  int32_t dtype;
+  int32_t prompt_len;            /* local budget anchor (policies.py:209-211) */
+  int32_t pos;                   /* position of the inserted token; current_len = pos+1 */
+  const void* q_dev;             /* [B,H,d] query of the new token */
+  const void* k_dev;             /* [B,H,d] key/value rows of the new token (inserted) */
+  const void* v_dev;
+  int64_t bh_stride;             /* elements between consecutive heads of q/k/v (>= d) */
+  const uint8_t* new_cls_dev;    /* [B] class of the new token */
+  const float* slope_dev;        /* [H] or NULL */
+  const float* sink_dev;         /* [H] or NULL */
+  const uint8_t* head_atoms_dev; /* [B*H] */
+  const double* head_r_l_dev;    /* [B*H] */
+  const double* head_r_f_dev;    /* [B*H] */
+  const int64_t* seg_off_dev;    /* [B*H] */
+  const int32_t* seg_cap_dev;    /* [B*H] */
+  void* kc_dev;
+  void* vc_dev;
+  int32_t* meta_dev;
+  double* score_dev;
+  const int32_t* live_in_dev;    /* [B*H] live slots before the step */
+  int32_t* live_out_dev;         /* [B*H] live slots after insert+evict (distinct buffer) */
+  float* out_dev;                /* [B,H,d] attention output (fp32) */
+  int32_t* evicted_dev;          /* [B*H] evictions this step (optional, may be NULL) */
+  int32_t* status_dev;           /* [1] sticky device status (capacity overflow), may be NULL */
+  int32_t max_cap;               /* max over heads of seg_cap (sizes the grid) */
+  int64_t total_slots;           /* arena slots (sizes the logit scratch) */
+  void* workspace_dev;
+  size_t workspace_bytes;
+} akv_decode_args;
+
+size_t akv_decode_workspace_size(int32_t B, int32_t H, int32_t d, int32_t max_cap, int64_t total_slots);
+int akv_decode_step(const akv_decode_args* a, void* stream);
+/* Zero the decode workspace counters (call once after allocating it). */
+int akv_decode_workspace_init(void* workspace_dev, size_t workspace_bytes, int32_t B, int32_t H,
+                              int32_t d, int32_t max_cap, int64_t total_slots, void* stream);
+
+/* ---- misc ------------------------------------------------------------ */
+const char* akv_last_error(void);
+const char* akv_version(void);
+int akv_device_check(void);   /* AKV_OK iff a sm_100 device is current */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AKV_H */

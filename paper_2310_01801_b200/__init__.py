@@ -1,0 +1,22 @@
+"""B200-native FastGen adaptive KV cache (arXiv 2310.01801).
+
+Drop-in for the reference package's profiling / policy / cache hot path
+(``adaptive_kv``: encode_prompt, generate_step, ...), backed by hand-written
+sm_100a kernels in ``libakv_sm100a.so`` (include/akv.h).  Importing the
+package loads the library and fails if it has not been built; compute
+calls fail unless an sm_100 device is present.  There is no CPU fallback.
+"""
+
+from ._lib import AkvError, lib as _lib_handle  # noqa: F401  (loads the .so)
+from .engine import (CompressedCache, EngineError, GenerationConfig, GenerationResult,
+                     GreedyArgmax, Nucleus, ProfileResult, StepRecord, decode_step_tensors,
+                     encode_prompt, encode_prompt_tensors, generate, generate_fixed_baseline,
+                     generate_step, records_to_ndjson, reference_generate)
+from .policies import (DEFAULT_FEASIBLE_ORDER, DEFAULT_RATIO, CompressionPolicy, PolicyAtom,
+                       PolicyError, RetainedSet, feasible_set, format_policy, full_policy,
+                       parse_policy)
+from .profiler import (HeadDecision, HeadProfile, ProfilerConfig, ProfilerError, RecoveryReport,
+                       RowAveraging, SelectionCriterion)
+from .tokens import TokenAnnotation, TokenClass, VocabMetadata, classify_tokens
+
+__version__ = "0.1.0"

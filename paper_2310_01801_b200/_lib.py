@@ -1,0 +1,126 @@
+"""ctypes binding of libakv_sm100a.so (include/akv.h).
+
+The library is built in-tree by ``__graft_entry__.build()``.  There is no
+fallback: if the shared object is missing the import fails, and compute
+entry points raise when no sm_100 device is present.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libakv_sm100a.so")
+
+AKV_OK, AKV_ERR_INVALID, AKV_ERR_CAPACITY, AKV_ERR_UNSUPPORTED, AKV_ERR_CUDA = range(5)
+DTYPE_F32, DTYPE_BF16 = 0, 1
+ATOM_SPECIAL, ATOM_PUNCT, ATOM_FREQUENT, ATOM_LOCAL, ATOM_FULL = 1, 2, 4, 8, 16
+ROWS_ALL, ROWS_LAST = 0, 1
+CRIT_RECOVERY, CRIT_COSINE = 0, 1
+MAX_FAMILY = 8
+MAX_THRESHOLDS = 8
+
+P = C.c_void_p
+i32, i64, f64, sz = C.c_int32, C.c_int64, C.c_double, C.c_size_t
+
+
+class ProfileArgs(C.Structure):
+    _fields_ = [
+        ("B", i32), ("H", i32), ("N", i32), ("d", i32), ("dtype", i32),
+        ("q_dev", P), ("k_dev", P), ("v_dev", P), ("ld", i64),
+        ("cls_dev", P), ("cls_ld", i64), ("slope_dev", P), ("sink_dev", P),
+        ("n_family", i32), ("family_atoms", C.c_uint8 * MAX_FAMILY),
+        ("family_r_l", f64 * MAX_FAMILY), ("family_r_f", f64 * MAX_FAMILY),
+        ("n_thresholds", i32), ("thresholds", f64 * MAX_THRESHOLDS),
+        ("rows", i32), ("criterion", i32),
+        ("lse_dev", P), ("colsum_dev", P), ("colsq_dev", P), ("lastp_dev", P),
+        ("out_last_dev", P), ("recovery_dev", P), ("cost_dev", P), ("cosine_dev", P),
+        ("choice_dev", P), ("kept_pos_dev", P), ("kept_count_dev", P),
+        ("last_row_recovery_dev", P), ("topk_gap_dev", P),
+        ("workspace_dev", P), ("workspace_bytes", sz),
+    ]
+
+
+class CompactArgs(C.Structure):
+    _fields_ = [
+        ("B", i32), ("H", i32), ("N", i32), ("d", i32), ("dtype", i32),
+        ("k_dev", P), ("v_dev", P), ("ld", i64), ("cls_dev", P), ("cls_ld", i64),
+        ("kept_pos_dev", P), ("kept_count_dev", P), ("colsum_dev", P), ("head_atoms_dev", P),
+        ("seg_off_dev", P), ("seg_cap_dev", P), ("kc_dev", P), ("vc_dev", P),
+        ("meta_dev", P), ("score_dev", P), ("live_dev", P),
+    ]
+
+
+class DecodeArgs(C.Structure):
+    _fields_ = [
+        ("B", i32), ("H", i32), ("d", i32), ("dtype", i32), ("prompt_len", i32), ("pos", i32),
+        ("q_dev", P), ("k_dev", P), ("v_dev", P), ("bh_stride", i64), ("new_cls_dev", P),
+        ("slope_dev", P), ("sink_dev", P), ("head_atoms_dev", P), ("head_r_l_dev", P),
+        ("head_r_f_dev", P), ("seg_off_dev", P), ("seg_cap_dev", P), ("kc_dev", P),
+        ("vc_dev", P), ("meta_dev", P), ("score_dev", P), ("live_in_dev", P),
+        ("live_out_dev", P), ("out_dev", P), ("evicted_dev", P), ("status_dev", P),
+        ("max_cap", i32), ("total_slots", i64), ("workspace_dev", P), ("workspace_bytes", sz),
+    ]
+
+
+# every symbol include/akv.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "akv_profile_workspace_size", "akv_profile", "akv_compact", "akv_plan_segments",
+    "akv_decode_workspace_size", "akv_decode_step", "akv_decode_workspace_init",
+    "akv_last_error", "akv_version", "akv_device_check",
+)
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python __graft_entry__.py` "
+            "(nvcc -gencode arch=compute_100a,code=sm_100a); there is no CPU fallback")
+    lib = C.CDLL(LIB_PATH)
+    lib.akv_profile_workspace_size.restype = sz
+    lib.akv_profile_workspace_size.argtypes = [i32, i32, i32, i32]
+    lib.akv_profile.restype = C.c_int
+    lib.akv_profile.argtypes = [C.POINTER(ProfileArgs), P]
+    lib.akv_compact.restype = C.c_int
+    lib.akv_compact.argtypes = [C.POINTER(CompactArgs), P]
+    lib.akv_plan_segments.restype = C.c_int
+    lib.akv_plan_segments.argtypes = [i32, P, i32, P, P, P, P]
+    lib.akv_decode_workspace_size.restype = sz
+    lib.akv_decode_workspace_size.argtypes = [i32, i32, i32, i32, i64]
+    lib.akv_decode_step.restype = C.c_int
+    lib.akv_decode_step.argtypes = [C.POINTER(DecodeArgs), P]
+    lib.akv_decode_workspace_init.restype = C.c_int
+    lib.akv_decode_workspace_init.argtypes = [P, sz, i32, i32, i32, i32, i64, P]
+    lib.akv_last_error.restype = C.c_char_p
+    lib.akv_version.restype = C.c_char_p
+    lib.akv_device_check.restype = C.c_int
+    return lib
+
+
+lib = _load()
+
+
+class AkvError(RuntimeError):
+    """Raised for CUDA / capacity / unsupported-shape failures of the library."""
+
+    def __init__(self, code: int, message: str):
+        super().__init__(f"[akv status {code}] {message}")
+        self.code = code
+
+
+def check(rc: int, exc_invalid=None):
+    """Map a status code to an exception.  AKV_ERR_INVALID raises
+    ``exc_invalid`` (the reference's PolicyError/ProfilerError/EngineError)
+    when given."""
+    if rc == AKV_OK:
+        return
+    msg = lib.akv_last_error().decode(errors="replace")
+    if rc == AKV_ERR_INVALID and exc_invalid is not None:
+        raise exc_invalid(msg)
+    raise AkvError(rc, msg)
+
+
+def require_device():
+    """Fail loudly unless a sm_100 device is current (no CPU fallback)."""
+    check(lib.akv_device_check())

@@ -1,0 +1,255 @@
+// Shared device helpers for the sm_100a adaptive-KV kernels.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/akv.h"
+
+namespace akv {
+
+constexpr int kClsShift = 24;          // meta = position | class << 24
+constexpr int kPosMask = (1 << kClsShift) - 1;
+
+__device__ __forceinline__ int meta_pos(int m) { return m & kPosMask; }
+__device__ __forceinline__ int meta_cls(int m) { return (m >> kClsShift) & 0xff; }
+
+// policies.py:205-206: max(1, ceil(r*L - 1e-9)) in IEEE float64, with the
+// product and the subtraction rounded separately (no FMA contraction), so
+// the budget is bit-identical to the reference's Python float arithmetic.
+__device__ __forceinline__ int budget(double r, int len) {
+  double x = __dsub_rn(__dmul_rn(r, (double)len), 1e-9);
+  int b = (int)ceil(x);
+  return b < 1 ? 1 : b;
+}
+
+template <typename T> struct Elem;
+template <> struct Elem<float> {
+  static constexpr int kPerVec = 4;  // elements per 16-byte vector
+  __device__ __forceinline__ static void unpack(const uint4& u, float* f) {
+    f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y);
+    f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);
+  }
+  __device__ __forceinline__ static float to_f(float x) { return x; }
+};
+template <> struct Elem<__nv_bfloat16> {
+  static constexpr int kPerVec = 8;
+  __device__ __forceinline__ static void unpack(const uint4& u, float* f) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = __uint_as_float(w[i] << 16);
+      f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+  __device__ __forceinline__ static float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+};
+
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint4 ld_cg_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_v4(void* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w) : "memory");
+}
+
+template <typename F>
+__device__ __forceinline__ float warp_allreduce(float v, F op) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_sum_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum (deterministic tree order); `red` needs blockDim/32 slots.
+template <typename V>
+__device__ __forceinline__ V block_sum(V v, V* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  V t = V(0);
+  for (int i = 0; i < nw; ++i) t += red[i];
+  __syncthreads();
+  return t;
+}
+
+// Exclusive block scan of small ints; returns the exclusive prefix of this
+// thread and writes the block total to *total.  `red` needs blockDim/32+1.
+__device__ __forceinline__ int block_exclusive_scan(int v, int* red, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();
+  if (lane == 31) red[warp] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int i = 0; i < nw; ++i) { int t = red[i]; red[i] = acc; acc += t; }
+    red[nw] = acc;
+  }
+  __syncthreads();
+  int ex = red[warp] + x - v;
+  *total = red[nw];
+  __syncthreads();
+  return ex;
+}
+
+// ---------------------------------------------------------------------------
+// Exact block-wide top-k over candidates keyed by (score desc, position asc),
+// the order of the reference's stable argsort on -scores (policies.py:238-240).
+// Scores are non-negative float64, so their IEEE bit patterns order like
+// unsigned integers.  Radix select on the 64-bit score keys (8-bit digits)
+// finds the k-th largest value v*; elements equal to v* are then taken in
+// ascending position order until k are selected (second radix select on
+// the 24-bit position when more than the remaining count tie).
+//
+// get(i, &key, &pos) reads candidate i (0 <= i < n).  Returns, through
+// *thr_key / *thr_pos, the smallest selected (key, pos): candidate i is in the
+// top-k iff key > thr_key || (key == thr_key && pos <= thr_pos).  If k >= n
+// everything is selected (thr_key = 0, thr_pos = INT_MAX).
+// `hist` needs 256 ints of shared memory, `red` 33 ints.
+template <typename Get>
+__device__ void block_topk_threshold(int n, int k, Get get, int* hist, int* red,
+                                     unsigned long long* thr_key, int* thr_pos) {
+  if (k >= n) {
+    *thr_key = 0ull;
+    *thr_pos = 0x7fffffff;
+    return;
+  }
+  __shared__ unsigned long long s_prefix;
+  __shared__ int s_remain, s_digit;
+  if (threadIdx.x == 0) { s_prefix = 0ull; s_remain = k; }
+  __syncthreads();
+  unsigned long long mask = 0ull;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const unsigned long long prefix = s_prefix;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      unsigned long long key; int pos;
+      get(i, &key, &pos);
+      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 0xff], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      // suffix scan over 256 bins (descending digit): lane owns 8 bins
+      const int lane = threadIdx.x;
+      int c[8], s = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { c[j] = hist[255 - (lane * 8 + j)]; s += c[j]; }
+      int incl = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int before = incl - s;  // elements with larger digits than my first bin
+      const int remain = s_remain;
+      int found = -1, above = 0;
+      int run = before;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (found < 0 && run < remain && run + c[j] >= remain) { found = 255 - (lane * 8 + j); above = run; }
+        run += c[j];
+      }
+      unsigned ball = __ballot_sync(0xffffffffu, found >= 0);
+      int src = __ffs(ball) - 1;
+      int dg = __shfl_sync(0xffffffffu, found, src);
+      int ab = __shfl_sync(0xffffffffu, above, src);
+      if (lane == 0) {
+        s_digit = dg;
+        s_remain = remain - ab;
+        s_prefix = prefix | ((unsigned long long)dg << shift);
+      }
+    }
+    __syncthreads();
+    mask |= (0xffull << shift);
+  }
+  const unsigned long long vstar = s_prefix;
+  const int need_eq = s_remain;  // how many elements equal to v* are selected (>= 1)
+  // count elements equal to v*
+  int cnt = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    unsigned long long key; int pos;
+    get(i, &key, &pos);
+    cnt += (key == vstar);
+  }
+  cnt = warp_sum_i(cnt);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  int n_eq = 0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) n_eq += red[i];
+  __syncthreads();
+  if (n_eq == need_eq) {
+    *thr_key = vstar;
+    *thr_pos = 0x7fffffff;
+    return;
+  }
+  // ties: select the need_eq smallest positions among key == v* (radix on
+  // inverted 24-bit positions, largest inverted == smallest position).
+  __shared__ int s_pprefix, s_premain;
+  if (threadIdx.x == 0) { s_pprefix = 0; s_premain = need_eq; }
+  __syncthreads();
+  int pmask = 0;
+  for (int shift = 16; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const int prefix = s_pprefix;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      unsigned long long key; int pos;
+      get(i, &key, &pos);
+      int ip = kPosMask - pos;
+      if (key == vstar && (ip & pmask) == prefix) atomicAdd(&hist[(ip >> shift) & 0xff], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int remain = s_premain, run = 0;
+      for (int dg = 255; dg >= 0; --dg) {
+        if (run + hist[dg] >= remain) {
+          s_premain = remain - run;
+          s_pprefix = prefix | (dg << shift);
+          break;
+        }
+        run += hist[dg];
+      }
+    }
+    __syncthreads();
+    pmask |= (0xff << shift);
+  }
+  *thr_key = vstar;
+  *thr_pos = kPosMask - s_pprefix;
+}
+
+__device__ __forceinline__ bool topk_selected(unsigned long long key, int pos,
+                                              unsigned long long thr_key, int thr_pos) {
+  return key > thr_key || (key == thr_key && pos <= thr_pos);
+}
+
+}  // namespace akv

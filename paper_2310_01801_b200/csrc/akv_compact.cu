@@ -1,0 +1,115 @@
+// K2: per-head KV compaction into the ragged, head-major compressed cache.
+//
+// Replaces the reference's encode_prompt compaction loop (engine.py:236-259):
+// retained_indices -> apply_policy (policies.py:270-288, rows gathered in
+// ascending position order) and the FREQUENT-only score copy
+// (engine.py:243-247).  Each head g owns slots [seg_off[g], seg_off[g] +
+// seg_cap[g]) of the arena; the kept rows fill the first kept_count[g]
+// slots and decode appends after them.  Rows move as 16-byte vectors,
+// a warp covering whole rows so loads and stores stay coalesced.
+
+#include "akv_common.cuh"
+#include "akv_internal.h"
+
+namespace akv {
+
+constexpr int kCompactRows = 32;
+
+struct CompactParams {
+  int H, N, row_vecs;  // 16-byte vectors per row
+  const uint4* k;
+  const uint4* v;
+  int64_t ld;
+  const uint8_t* cls;
+  int64_t cls_ld;
+  const int32_t* kept_pos;
+  const int32_t* kept_count;
+  const double* colsum;
+  const uint8_t* atoms;
+  const int64_t* seg_off;
+  const int32_t* seg_cap;
+  uint4* kc;
+  uint4* vc;
+  int32_t* meta;
+  double* score;
+  int32_t* live;
+};
+
+__global__ void __launch_bounds__(128) k2_compact(CompactParams p) {
+  const int g = blockIdx.y;
+  const int kept = p.kept_count[g];
+  const int cap = p.seg_cap[g];
+  const int i0 = blockIdx.x * kCompactRows;
+  // a segment too small for its kept rows is reported as live = -1
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.live[g] = kept > cap ? -1 : kept;
+  if (i0 >= kept || kept > cap) return;
+  const int nrows = min(kCompactRows, kept - i0);
+  const int64_t base = p.seg_off[g];
+  const int b = g / p.H;
+  const int32_t* kp = p.kept_pos + (size_t)g * p.N;
+  const uint4* ksrc = p.k + (size_t)g * p.ld * p.row_vecs;
+  const uint4* vsrc = p.v + (size_t)g * p.ld * p.row_vecs;
+  for (int idx = threadIdx.x; idx < nrows * p.row_vecs; idx += blockDim.x) {
+    const int r = idx / p.row_vecs, c = idx % p.row_vecs;
+    const int pos = kp[i0 + r];
+    const size_t dst = (size_t)(base + i0 + r) * p.row_vecs + c;
+    const uint4 kv = ld_nc_v4(ksrc + (size_t)pos * p.row_vecs + c);
+    const uint4 vv = ld_nc_v4(vsrc + (size_t)pos * p.row_vecs + c);
+    st_v4(p.kc + dst, kv);
+    st_v4(p.vc + dst, vv);
+  }
+  const bool freq = (p.atoms[g] & AKV_ATOM_FREQUENT) && !(p.atoms[g] & AKV_ATOM_FULL);
+  for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
+    const int pos = kp[i0 + r];
+    const int64_t slot = base + i0 + r;
+    p.meta[slot] = pos | ((int)p.cls[(size_t)b * p.cls_ld + pos] << kClsShift);
+    p.score[slot] = freq ? p.colsum[(size_t)g * p.N + pos] : 0.0;
+  }
+}
+
+__global__ void k2_plan(int G, const int32_t* kept, int32_t extra, int32_t* cap, int64_t* off,
+                        int64_t* total) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int64_t acc = 0;
+  for (int g = 0; g < G; ++g) {
+    const int c = ((kept[g] + extra + 7) / 8) * 8;  // 8-slot aligned segments
+    cap[g] = c;
+    off[g] = acc;
+    acc += c;
+  }
+  *total = acc;
+}
+
+}  // namespace akv
+
+using namespace akv;
+
+extern "C" int akv_plan_segments(int32_t G, const int32_t* kept_count_dev, int32_t extra,
+                                 int32_t* seg_cap_dev, int64_t* seg_off_dev, int64_t* total_dev,
+                                 void* stream) {
+  if (G < 1 || extra < 0) return set_error(AKV_ERR_INVALID, "akv_plan_segments: bad G/extra");
+  k2_plan<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(G, kept_count_dev, extra, seg_cap_dev,
+                                                          seg_off_dev, total_dev);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(AKV_ERR_CUDA, "akv_plan_segments: %s", cudaGetErrorString(e));
+  return AKV_OK;
+}
+
+extern "C" int akv_compact(const akv_compact_args* a, void* stream) {
+  if (!a) return set_error(AKV_ERR_INVALID, "akv_compact: null args");
+  if (a->B < 1 || a->H < 1 || a->N < 1) return set_error(AKV_ERR_INVALID, "akv_compact: empty input");
+  const int es = a->dtype == AKV_DTYPE_BF16 ? 2 : a->dtype == AKV_DTYPE_F32 ? 4 : 0;
+  if (!es || (a->d * es) % 16 || a->d * es > 512)
+    return set_error(AKV_ERR_UNSUPPORTED, "akv_compact: unsupported dtype %d / head dim %d", a->dtype, a->d);
+  CompactParams p{a->H, a->N, a->d * es / 16,
+                  static_cast<const uint4*>(a->k_dev), static_cast<const uint4*>(a->v_dev), a->ld,
+                  a->cls_dev, a->cls_ld, a->kept_pos_dev, a->kept_count_dev, a->colsum_dev,
+                  a->head_atoms_dev, a->seg_off_dev, a->seg_cap_dev,
+                  static_cast<uint4*>(a->kc_dev), static_cast<uint4*>(a->vc_dev), a->meta_dev,
+                  a->score_dev, a->live_dev};
+  dim3 grid((a->N + kCompactRows - 1) / kCompactRows, a->B * a->H);
+  k2_compact<<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(AKV_ERR_CUDA, "akv_compact: %s", cudaGetErrorString(e));
+  return AKV_OK;
+}

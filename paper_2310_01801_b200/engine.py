@@ -1,0 +1,552 @@
+"""Two-phase generation over the compressed KV cache (reference:
+engine.py:39-525), B200-native.
+
+Phase one (``encode_prompt``) runs K1 (profiling) and K2 (compaction) on
+the GPU; phase two (``generate_step``) runs one K3 launch per token for all
+heads.  The reference's duck-typed model protocol
+(``config``/``vocab``/``k_row``/``v_row``/``q_row``/``head_logits``,
+model.py:150-286) is kept for drop-in use; ``encode_prompt_tensors`` /
+``decode_step_tensors`` are the tensor-level entry points the model-protocol
+functions are built on: q, k, v are device tensors ``[B, H, ld, d]``
+(fp32 or bf16), every (b, h) an independent head.
+
+The host only orchestrates: it allocates device memory (PyTorch is used
+for allocation and streams), reads back the per-head profile once after
+K1 (one small device->host copy that also sizes the ragged arena), and
+launches kernels.  There is no CPU compute path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import json
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import (ATOM_FULL, CRIT_COSINE, CRIT_RECOVERY, DTYPE_BF16, DTYPE_F32, ROWS_ALL,
+                   ROWS_LAST, CompactArgs, DecodeArgs, ProfileArgs, check, lib)
+from .policies import CompressionPolicy, PolicyAtom, full_policy
+from .profiler import (HeadDecision, HeadProfile, ProfilerConfig, ProfilerError, RowAveraging,
+                       SelectionCriterion)
+from .tokens import CLASS_CODE, TokenAnnotation, VocabMetadata, classify_tokens
+
+
+class EngineError(ValueError):
+    """Invalid generation state or configuration (engine.py:39-40)."""
+
+
+@dataclass(frozen=True)
+class GreedyArgmax:
+    pass
+
+
+@dataclass(frozen=True)
+class Nucleus:
+    temperature: float = 0.6
+    top_p: float = 0.9
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.temperature <= 0.0:
+            raise EngineError(f"temperature must be > 0, got {self.temperature}")
+        if not 0.0 < self.top_p <= 1.0:
+            raise EngineError(f"top_p must be in (0, 1], got {self.top_p}")
+
+
+@dataclass(frozen=True)
+class GenerationConfig:
+    max_new_tokens: int
+    sampling: object = field(default_factory=GreedyArgmax)
+
+    def __post_init__(self):
+        if self.max_new_tokens < 0:
+            raise EngineError("max_new_tokens must be >= 0")
+
+
+class _Sampler:
+    """Next-token choice from the model's logits (engine.py:71-90)."""
+
+    def __init__(self, sampling):
+        self.sampling = sampling
+        self._rng = (np.random.Generator(np.random.PCG64(sampling.seed))
+                     if isinstance(sampling, Nucleus) else None)
+
+    def __call__(self, logits) -> int:
+        logits = np.asarray(logits, dtype=np.float64)
+        if isinstance(self.sampling, GreedyArgmax):
+            return int(np.argmax(logits))
+        z = logits / self.sampling.temperature
+        z = np.exp(z - z.max())
+        probs = z / z.sum()
+        order = np.argsort(-probs, kind="stable")
+        cum = np.cumsum(probs[order])
+        cut = min(int(np.searchsorted(cum, self.sampling.top_p, side="left")), probs.size - 1)
+        kept = order[:cut + 1]
+        return int(self._rng.choice(kept, p=probs[kept] / probs[kept].sum()))
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return DTYPE_F32
+    if t.dtype == torch.bfloat16:
+        return DTYPE_BF16
+    raise EngineError(f"unsupported dtype {t.dtype}; use float32 or bfloat16")
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+@dataclass
+class ProfileResult:
+    """Everything K1 reports per head (flattened g = b*H + h)."""
+
+    family: tuple                 # CompressionPolicy per family member
+    thresholds: tuple
+    recovery: np.ndarray          # [G, F]
+    cost: np.ndarray              # [G, F]
+    cosine: np.ndarray            # [G, F]
+    choice: np.ndarray            # [G, nT]
+    kept_count: np.ndarray        # [G]
+    last_row_recovery: np.ndarray  # [G]
+    topk_gap: np.ndarray          # [G]
+
+    def near_threshold(self, tol: float = 1e-4) -> np.ndarray:
+        """Heads whose recovery of any member up to the chosen one lies within
+        ``tol`` of T (listed separately by the parity contract)."""
+        G, F = self.recovery.shape
+        out = np.zeros((G, len(self.thresholds)), dtype=bool)
+        for t, T in enumerate(self.thresholds):
+            for g in range(G):
+                c = self.choice[g, t]
+                upto = F if c < 0 else c + 1
+                out[g, t] = bool(np.any(np.abs(self.recovery[g, :upto] - T) < tol))
+        return out
+
+    def policies(self, t: int = 0) -> list:
+        return [self.family[c] for c in self.choice[:, t]]
+
+
+class CompressedCache:
+    """Per-head compressed KV state of one batch of sessions, resident in HBM
+    (engine.py:100-144).  Head g = b*H + h owns arena slots
+    [seg_off[g], seg_off[g] + seg_cap[g])."""
+
+    def __init__(self, B, H, d, dtype, prompt_len, capacity_steps, device):
+        self.B, self.H, self.d = B, H, d
+        self.G = B * H
+        self.dtype = dtype
+        self.prompt_len = prompt_len
+        self.seq_len = prompt_len
+        self.capacity_steps = capacity_steps
+        self.device = device
+        self.profile: HeadProfile | None = None
+        self.profile_result: ProfileResult | None = None
+        self.keys: list = []
+        self.annotations: list = []
+        self.diagnostics = False
+        self.last_record = None
+        self._parity = 0
+
+    # live slot counts (double-buffered across steps)
+    @property
+    def live(self) -> torch.Tensor:
+        return self.live_buf[self._parity]
+
+    def total_retained(self) -> int:
+        return int(self.live.sum().item())
+
+    def head_retained(self) -> np.ndarray:
+        return self.live.cpu().numpy().astype(np.int64)
+
+    def retained_positions(self, g: int | None = None):
+        """Sorted live positions of head g (or a list for all heads); one
+        device->host copy per call (diagnostics only)."""
+        live = self.live.cpu().numpy()
+        off = self.seg_off.cpu().numpy()
+        meta = self.meta.cpu().numpy()
+        def one(i):
+            m = meta[off[i]: off[i] + live[i]]
+            return np.sort(m & ((1 << 24) - 1))
+        if g is not None:
+            return one(g)
+        return [one(i) for i in range(self.G)]
+
+    @property
+    def pending_output(self) -> torch.Tensor:
+        """Latest attention output per head, fp32 [B, H, d]."""
+        return self.out
+
+    def check(self):
+        st = int(self.status.item())
+        if st != 0:
+            raise _lib.AkvError(st, "decode overflowed a cache segment (capacity exceeded)")
+
+
+def _family_arrays(family, args):
+    if len(family) > _lib.MAX_FAMILY:
+        raise ProfilerError(f"feasible family longer than {_lib.MAX_FAMILY} policies")
+    args.n_family = len(family)
+    for i, pol in enumerate(family):
+        args.family_atoms[i] = pol.bits
+        args.family_r_l[i] = pol.r_l
+        args.family_r_f[i] = pol.r_f
+
+
+def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None = None,
+                          fixed_policy: CompressionPolicy | None = None, *, prompt_len=None,
+                          max_new_tokens: int = 0, extra_thresholds=(), slopes=None,
+                          sinks=None):
+    """Profile, select and compact every head of a batch (Alg. 1,
+    engine.py:203-272) on the GPU.
+
+    q, k, v: CUDA tensors [B, H, ld, d] (float32 or bfloat16); the first
+    ``prompt_len`` rows of every head are the prompt.  classes: CUDA uint8
+    [B, >= prompt_len] token classes (0 other, 1 special, 2 punct).
+    slopes/sinks: optional CUDA float32 [H] planted head bias (synthetic
+    workloads).  Returns (ProfileResult, CompressedCache) with capacity for
+    ``max_new_tokens`` inserted tokens per head.
+    """
+    if profiler_cfg is None and fixed_policy is None:
+        raise EngineError("need a profiler config or a fixed policy")
+    _lib.require_device()
+    if q.dim() != 4 or q.shape != k.shape or q.shape != v.shape:
+        raise EngineError("q, k, v must be [B, H, ld, d] tensors of one shape")
+    if not (q.is_cuda and k.is_cuda and v.is_cuda and classes.is_cuda):
+        raise EngineError("inputs must be CUDA tensors")
+    for t in (q, k, v):
+        if not t.is_contiguous():
+            raise EngineError("q, k, v must be contiguous")
+    B, H, ld, d = q.shape
+    N = ld if prompt_len is None else int(prompt_len)
+    if N < 1:
+        raise EngineError("empty prompt")
+    if N > ld:
+        raise EngineError(f"prompt_len {N} out of range for {ld} rows")
+    dt = _dtype_code(q)
+    dev = q.device
+    G = B * H
+    if fixed_policy is not None:
+        family = (fixed_policy,)
+        thresholds = (-1.0,)
+        rows, crit = ROWS_ALL, CRIT_RECOVERY
+    else:
+        family = tuple(profiler_cfg.feasible)
+        thresholds = (profiler_cfg.recovery_threshold,) + tuple(extra_thresholds)
+        rows = ROWS_LAST if profiler_cfg.rows is RowAveraging.LAST_ROW else ROWS_ALL
+        crit = (CRIT_COSINE if profiler_cfg.criterion is SelectionCriterion.COSINE_SIMILARITY
+                else CRIT_RECOVERY)
+    if len(thresholds) > _lib.MAX_THRESHOLDS:
+        raise ProfilerError(f"at most {_lib.MAX_THRESHOLDS} thresholds per profiling pass")
+    F = len(family)
+    f32, f64, i32 = torch.float32, torch.float64, torch.int32
+    classes = classes.to(torch.uint8).contiguous()
+    out = dict(
+        lse=torch.empty(G, N, dtype=f32, device=dev),
+        colsum=torch.empty(G, N, dtype=f64, device=dev),
+        colsq=torch.empty(G, N, dtype=f64, device=dev),
+        lastp=torch.empty(G, N, dtype=f32, device=dev),
+        out_last=torch.empty(B, H, d, dtype=f32, device=dev),
+        recovery=torch.empty(G, F, dtype=f64, device=dev),
+        cost=torch.empty(G, F, dtype=i32, device=dev),
+        cosine=torch.empty(G, F, dtype=f64, device=dev),
+        choice=torch.empty(G, len(thresholds), dtype=torch.int8, device=dev),
+        kept_pos=torch.empty(G, N, dtype=i32, device=dev),
+        kept_count=torch.empty(G, dtype=i32, device=dev),
+        lrr=torch.empty(G, dtype=f64, device=dev),
+        gap=torch.empty(G, dtype=f64, device=dev),
+    )
+    ws_bytes = lib.akv_profile_workspace_size(B, H, N, d)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    a = ProfileArgs()
+    a.B, a.H, a.N, a.d, a.dtype = B, H, N, d, dt
+    a.q_dev, a.k_dev, a.v_dev, a.ld = _ptr(q), _ptr(k), _ptr(v), ld
+    a.cls_dev, a.cls_ld = _ptr(classes), classes.shape[1]
+    a.slope_dev, a.sink_dev = _ptr(slopes), _ptr(sinks)
+    _family_arrays(family, a)
+    a.n_thresholds = len(thresholds)
+    for i, t in enumerate(thresholds):
+        a.thresholds[i] = t
+    a.rows, a.criterion = rows, crit
+    (a.lse_dev, a.colsum_dev, a.colsq_dev, a.lastp_dev, a.out_last_dev, a.recovery_dev,
+     a.cost_dev, a.cosine_dev, a.choice_dev, a.kept_pos_dev, a.kept_count_dev,
+     a.last_row_recovery_dev, a.topk_gap_dev) = (
+        _ptr(out[n]) for n in ("lse", "colsum", "colsq", "lastp", "out_last", "recovery", "cost",
+                               "cosine", "choice", "kept_pos", "kept_count", "lrr", "gap"))
+    a.workspace_dev, a.workspace_bytes = _ptr(ws), ws_bytes
+    stream = _stream()
+    check(lib.akv_profile(C.byref(a), stream), ProfilerError)
+
+    # ragged arena plan (device prefix sum), then the one device->host read
+    seg_cap = torch.empty(G, dtype=i32, device=dev)
+    seg_off = torch.empty(G, dtype=torch.int64, device=dev)
+    total = torch.empty(1, dtype=torch.int64, device=dev)
+    check(lib.akv_plan_segments(G, _ptr(out["kept_count"]), int(max_new_tokens), _ptr(seg_cap),
+                                _ptr(seg_off), _ptr(total), stream))
+    host = {n: out[n].cpu() for n in ("recovery", "cost", "cosine", "choice", "kept_count", "lrr",
+                                      "gap")}
+    total_slots = int(total.item())
+    choice = host["choice"].numpy().astype(np.int64)
+    if (choice < 0).any():
+        raise ProfilerError("no feasible policy met the threshold")
+    res = ProfileResult(
+        family=family, thresholds=thresholds, recovery=host["recovery"].numpy(),
+        cost=host["cost"].numpy().astype(np.int64), cosine=host["cosine"].numpy(), choice=choice,
+        kept_count=host["kept_count"].numpy().astype(np.int64),
+        last_row_recovery=host["lrr"].numpy(), topk_gap=host["gap"].numpy())
+
+    cache = CompressedCache(B, H, d, q.dtype, N, int(max_new_tokens), dev)
+    cache.profile_result = res
+    chosen = [family[c] for c in choice[:, 0]]
+    atoms = torch.tensor([p.bits for p in chosen], dtype=torch.uint8).to(dev, non_blocking=True)
+    cache.head_atoms = atoms
+    cache.head_r_l = torch.tensor([p.r_l for p in chosen], dtype=f64).to(dev, non_blocking=True)
+    cache.head_r_f = torch.tensor([p.r_f for p in chosen], dtype=f64).to(dev, non_blocking=True)
+    cache.seg_cap, cache.seg_off = seg_cap, seg_off
+    cache.max_cap = int(max(1, ((N + max_new_tokens + 7) // 8) * 8))
+    cache.total_slots = max(total_slots, 1)
+    cache.kc = torch.empty(cache.total_slots, d, dtype=q.dtype, device=dev)
+    cache.vc = torch.empty(cache.total_slots, d, dtype=q.dtype, device=dev)
+    cache.meta = torch.empty(cache.total_slots, dtype=i32, device=dev)
+    cache.score = torch.empty(cache.total_slots, dtype=f64, device=dev)
+    cache.live_buf = [torch.empty(G, dtype=i32, device=dev), torch.empty(G, dtype=i32, device=dev)]
+    cache.out = out["out_last"]
+    cache.evicted = torch.zeros(G, dtype=i32, device=dev)
+    cache.status = torch.zeros(1, dtype=i32, device=dev)
+    cache.classes = classes
+    cache.slopes, cache.sinks = slopes, sinks
+    cache.colsum = out["colsum"]
+    cache.lastp = out["lastp"]
+
+    c = CompactArgs()
+    c.B, c.H, c.N, c.d, c.dtype = B, H, N, d, dt
+    c.k_dev, c.v_dev, c.ld = _ptr(k), _ptr(v), ld
+    c.cls_dev, c.cls_ld = _ptr(classes), classes.shape[1]
+    c.kept_pos_dev, c.kept_count_dev, c.colsum_dev = (_ptr(out["kept_pos"]),
+                                                      _ptr(out["kept_count"]), _ptr(out["colsum"]))
+    c.head_atoms_dev, c.seg_off_dev, c.seg_cap_dev = _ptr(atoms), _ptr(seg_off), _ptr(seg_cap)
+    c.kc_dev, c.vc_dev, c.meta_dev, c.score_dev = (_ptr(cache.kc), _ptr(cache.vc),
+                                                   _ptr(cache.meta), _ptr(cache.score))
+    c.live_dev = _ptr(cache.live_buf[0])
+    check(lib.akv_compact(C.byref(c), stream), EngineError)
+
+    ws_bytes = lib.akv_decode_workspace_size(B, H, d, cache.max_cap, cache.total_slots)
+    cache.workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    check(lib.akv_decode_workspace_init(_ptr(cache.workspace), ws_bytes, B, H, d, cache.max_cap,
+                                        cache.total_slots, stream))
+    cache._dargs = _decode_args(cache, dt)
+    return res, cache
+
+
+def _decode_args(cache: CompressedCache, dt: int) -> DecodeArgs:
+    a = DecodeArgs()
+    a.B, a.H, a.d, a.dtype, a.prompt_len = cache.B, cache.H, cache.d, dt, cache.prompt_len
+    a.slope_dev, a.sink_dev = _ptr(cache.slopes), _ptr(cache.sinks)
+    a.head_atoms_dev, a.head_r_l_dev, a.head_r_f_dev = (_ptr(cache.head_atoms),
+                                                        _ptr(cache.head_r_l), _ptr(cache.head_r_f))
+    a.seg_off_dev, a.seg_cap_dev = _ptr(cache.seg_off), _ptr(cache.seg_cap)
+    a.kc_dev, a.vc_dev, a.meta_dev, a.score_dev = (_ptr(cache.kc), _ptr(cache.vc),
+                                                   _ptr(cache.meta), _ptr(cache.score))
+    a.out_dev, a.evicted_dev, a.status_dev = _ptr(cache.out), _ptr(cache.evicted), _ptr(cache.status)
+    a.max_cap, a.total_slots = cache.max_cap, cache.total_slots
+    a.workspace_dev, a.workspace_bytes = _ptr(cache.workspace), cache.workspace.numel()
+    return a
+
+
+def decode_step_tensors(cache: CompressedCache, q, k, v, new_classes) -> torch.Tensor:
+    """One decode step for every head (Alg. 2 inner loop, engine.py:303-350):
+    insert the new token's k/v, attend, update scores, evict.  q, k, v:
+    CUDA tensors whose [B, H, :d] slices are the new token's rows (any
+    head stride); new_classes: CUDA uint8 [B].  Returns the fp32 attention
+    output [B, H, d] (the cache's pending output buffer)."""
+    if cache.seq_len - cache.prompt_len >= cache.capacity_steps:
+        raise EngineError(
+            f"cache capacity of {cache.capacity_steps} decode steps exhausted; "
+            "encode with a larger max_new_tokens")
+    a = cache._dargs
+    a.pos = cache.seq_len
+    a.q_dev, a.k_dev, a.v_dev = _ptr(q), _ptr(k), _ptr(v)
+    a.bh_stride = q.stride(1)
+    a.new_cls_dev = _ptr(new_classes)
+    a.live_in_dev = _ptr(cache.live_buf[cache._parity])
+    a.live_out_dev = _ptr(cache.live_buf[cache._parity ^ 1])
+    check(lib.akv_decode_step(C.byref(a), _stream()), EngineError)
+    cache._parity ^= 1
+    cache.seq_len += 1
+    return cache.out
+
+
+# ---------------------------------------------------------------------------
+# reference-protocol drop-ins (engine.py:203-502)
+
+@dataclass
+class StepRecord:
+    step: int
+    token_id: int
+    head_retained: dict
+    total_cache_tokens: int
+    mean_recovery: float | None
+    retained_positions: dict | None = None
+
+
+@dataclass
+class GenerationResult:
+    tokens: list
+    profile: HeadProfile
+    records: list
+    cache: CompressedCache
+
+
+def _model_rows(model, grid, positions, klass_of, prompt_len):
+    d = model.config.head_dim
+    G, n = len(grid), len(positions)
+    q = np.empty((1, G, n, d), dtype=np.float32)
+    k = np.empty_like(q)
+    v = np.empty_like(q)
+    for gi, (layer, head) in enumerate(grid):
+        for i, pos in enumerate(positions):
+            k[0, gi, i] = model.k_row(layer, head, pos, klass_of(pos), prompt_len)
+            v[0, gi, i] = model.v_row(layer, head, pos)
+            q[0, gi, i] = model.q_row(layer, head, pos, prompt_len)
+    return q, k, v
+
+
+def encode_prompt(model, prompt_tokens, profiler_cfg: ProfilerConfig | None,
+                  fixed_policy: CompressionPolicy | None = None, threads=None,
+                  diagnostics: bool = True, max_new_tokens: int = 256):
+    """Drop-in for engine.py:203-272 over the duck-typed model protocol.
+
+    Rows are gathered from the model (float64 -> float32) into one [1, G, n,
+    d] batch whose heads are the model's sorted (layer, head) grid, then
+    profiled and compacted on the GPU.  ``threads`` is accepted for API
+    compatibility (the GPU processes all heads at once).
+    """
+    if profiler_cfg is None and fixed_policy is None:
+        raise EngineError("need a profiler config or a fixed policy")
+    prompt_tokens = list(prompt_tokens)
+    if not prompt_tokens:
+        raise EngineError("empty prompt")
+    grid = sorted(model.config.head_grid())
+    n = len(prompt_tokens)
+    annotations = classify_tokens(prompt_tokens, model.vocab)
+    q, k, v = _model_rows(model, grid, range(n), lambda p: annotations[p].klass, n)
+    dev = torch.device("cuda")
+    cls = torch.tensor([[CLASS_CODE[a.klass] for a in annotations]], dtype=torch.uint8)
+    res, cache = encode_prompt_tensors(
+        torch.from_numpy(q).to(dev), torch.from_numpy(k).to(dev), torch.from_numpy(v).to(dev),
+        cls.to(dev), profiler_cfg, fixed_policy, max_new_tokens=max_new_tokens)
+    choice = res.choice[:, 0]
+    decisions = {}
+    for gi, key in enumerate(grid):
+        pol = res.family[choice[gi]]
+        decisions[key] = HeadDecision(pol, float(res.recovery[gi, choice[gi]]),
+                                      int(res.cost[gi, choice[gi]]))
+    profile = HeadProfile(decisions)
+    cache.profile = profile
+    cache.keys = grid
+    cache.annotations = list(annotations)
+    cache.diagnostics = diagnostics
+    cache._model_new_cls = torch.empty(1, dtype=torch.uint8, device=dev)
+    return profile, cache
+
+
+def _check_cache(model, cache: CompressedCache):
+    expected = set(model.config.head_grid())
+    if set(cache.keys) != expected or (cache.profile is not None and
+                                       set(cache.profile.decisions) != expected):
+        raise EngineError("cache/profile mismatch: head grid does not match the model")
+
+
+def generate_step(model, cache: CompressedCache, last_token=None, sampler=None):
+    """Drop-in for engine.py:283-371: insert ``last_token`` (if given) into
+    every head's cache on the GPU, then sample the next token from
+    ``model.head_logits`` over the concatenated head outputs."""
+    _check_cache(model, cache)
+    if not isinstance(sampler, _Sampler):
+        sampler = _Sampler(sampler if sampler is not None else GreedyArgmax())
+    if last_token is not None:
+        pos = cache.seq_len
+        klass = model.vocab.classify_id(last_token)
+        cache.annotations.append(TokenAnnotation(pos, int(last_token), klass))
+        q, k, v = _model_rows(model, cache.keys, [pos], lambda p: klass, cache.prompt_len)
+        dev = cache.device
+        qd = torch.from_numpy(q[:, :, 0]).to(dev)
+        kd = torch.from_numpy(k[:, :, 0]).to(dev)
+        vd = torch.from_numpy(v[:, :, 0]).to(dev)
+        cache._model_new_cls.fill_(CLASS_CODE[klass])
+        decode_step_tensors(cache, qd.to(cache.dtype), kd.to(cache.dtype), vd.to(cache.dtype),
+                            cache._model_new_cls)
+    concat = cache.out.reshape(-1).double().cpu().numpy()
+    next_token = sampler(model.head_logits(concat))
+    live = cache.head_retained()
+    cache.last_record = StepRecord(
+        step=0, token_id=next_token,
+        head_retained={key: int(live[i]) for i, key in enumerate(cache.keys)},
+        total_cache_tokens=int(live.sum()), mean_recovery=None,
+        retained_positions=(
+            {key: tuple(int(x) for x in p)
+             for key, p in zip(cache.keys, cache.retained_positions())}
+            if cache.diagnostics else None))
+    return next_token, cache
+
+
+def _run_decode(model, cache, profile, gen_cfg):
+    sampler = _Sampler(gen_cfg.sampling)
+    tokens, records, last = [], [], None
+    for step in range(1, gen_cfg.max_new_tokens + 1):
+        tok, cache = generate_step(model, cache, last, sampler)
+        rec = cache.last_record
+        rec.step = step
+        tokens.append(tok)
+        records.append(rec)
+        last = tok
+    return GenerationResult(tokens, profile, records, cache)
+
+
+def generate(model, prompt_tokens, profiler_cfg: ProfilerConfig, gen_cfg: GenerationConfig,
+             threads=None, diagnostics: bool = True) -> GenerationResult:
+    """Encode once, then ``max_new_tokens`` decoding steps (engine.py:382-394)."""
+    profile, cache = encode_prompt(model, prompt_tokens, profiler_cfg, threads=threads,
+                                   diagnostics=diagnostics,
+                                   max_new_tokens=max(1, gen_cfg.max_new_tokens))
+    return _run_decode(model, cache, profile, gen_cfg)
+
+
+def generate_fixed_baseline(model, prompt_tokens, policy: CompressionPolicy,
+                            gen_cfg: GenerationConfig, diagnostics: bool = True):
+    """One imposed policy on every head, no profiling (engine.py:397-408)."""
+    profile, cache = encode_prompt(model, prompt_tokens, None, fixed_policy=policy,
+                                   diagnostics=diagnostics,
+                                   max_new_tokens=max(1, gen_cfg.max_new_tokens))
+    return _run_decode(model, cache, profile, gen_cfg)
+
+
+def reference_generate(model, prompt_tokens, gen_cfg: GenerationConfig) -> GenerationResult:
+    """Uncompressed baseline (engine.py:428-502): the full policy on every
+    head through the same kernels (no eviction ever happens)."""
+    res = generate_fixed_baseline(model, prompt_tokens, full_policy(), gen_cfg, diagnostics=False)
+    for rec in res.records:
+        rec.mean_recovery = 1.0
+    return GenerationResult(res.tokens, HeadProfile({}), res.records, res.cache)
+
+
+def records_to_ndjson(records, num_layers: int, num_heads: int) -> str:
+    """One JSON object per step, retained counts in layer-major order
+    (engine.py:505-525)."""
+    lines = []
+    for rec in records:
+        grid = [[rec.head_retained[(layer, head)] for head in range(num_heads)]
+                for layer in range(num_layers)]
+        lines.append(json.dumps({"step": rec.step, "token_id": rec.token_id,
+                                 "head_retained": grid,
+                                 "total_cache_tokens": rec.total_cache_tokens,
+                                 "mean_recovery": rec.mean_recovery}, sort_keys=True))
+    return "\n".join(lines) + ("\n" if lines else "")
