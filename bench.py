@@ -1,0 +1,456 @@
+#!/usr/bin/env python
+"""Benchmark of the FastGen adaptive-KV hot path on B200.
+
+Workload (BASELINE.json configs[1], the Llama-7B-shape layer): B=8, H=32,
+d=128, prompt N=1024, D=512 decode insertions, bf16, planted local/sink
+structure on a seeded 25% of heads, fixed T (default 0.95; the sweep T in
+{0.95, 0.98, 0.99} is reported too).  Synthetic seeded inputs (no dataset
+is available offline).
+
+One bench "step" = one full session over the batch: K1 profiling + K2
+compaction (with the single device->host read that sizes the ragged arena)
++ D K3 decode steps.  ``value`` = decode tokens/s over the whole session
+(B*D tokens / session time, profiling included).  The KV arena streamed by
+every decode step (~130-200 MB) is larger than the 126 MB L2.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Under torchrun every rank runs its own c1 batch (seed offset by rank; weak
+scaling, no data-path collective); rank 0 prints the JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except OSError:
+        return PEAKS_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in getattr(self, "lines", []):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def make_inputs(w, device):
+    import torch
+
+    from paper_2310_01801_b200.workloads import class_lut
+
+    q, k, v = w.qkv()
+    lut = class_lut()
+    cls = lut[w.all_tokens()]
+    t = lambda x: torch.from_numpy(x).to(device).to(torch.bfloat16 if w.dtype == "bf16" else torch.float32)
+    return (t(q), t(k), t(v), torch.from_numpy(cls).to(device), q, k, v, cls)
+
+
+def run_session(w, T, qd, kd, vd, cd, slopes, sinks, decode_inputs, ev=None, record=False):
+    """One session: encode (K1+K2) then D decode steps.  Returns the cache and,
+    when ``record``, the live slot counts before every decode step."""
+    import torch
+
+    from paper_2310_01801_b200 import ProfilerConfig, decode_step_tensors, encode_prompt_tensors
+
+    cfg = ProfilerConfig(recovery_threshold=T)
+    if ev is not None:
+        ev[0].record()
+    res, cache = encode_prompt_tensors(qd, kd, vd, cd, cfg, prompt_len=w.N, max_new_tokens=w.D,
+                                       slopes=slopes, sinks=sinks)
+    if ev is not None:
+        ev[1].record()
+    lives = []
+    dq, dk, dv, dc = decode_inputs
+    for t in range(w.D):
+        if record:
+            lives.append(cache.live.cpu().numpy().copy())
+        decode_step_tensors(cache, dq[t], dk[t], dv[t], dc[t])
+    if ev is not None:
+        ev[2].record()
+    if record:
+        lives.append(cache.live.cpu().numpy().copy())
+    return res, cache, lives
+
+
+def decode_bytes(w, res, lives):
+    """Algorithmic HBM bytes of each K3 launch: per head the
+    live K and V rows plus the new row, the 4-byte slot metadata, and for
+    FREQUENT heads the float64 score read+write; plus q/k/v in and o out."""
+    es = 2 if w.dtype == "bf16" else 4
+    fam = res.family
+    freq = np.array([bool(fam[c].bits & 4) and not fam[c].is_full for c in res.choice[:, 0]])
+    G = len(freq)
+    out = []
+    for L in lives[:-1]:
+        L = L.astype(np.int64)
+        b = ((L + 1) * (2 * w.d * es + 4)).sum() + (L[freq] * 16).sum()
+        b += G * (3 * w.d * es + w.d * 4)
+        out.append(int(b))
+    return out
+
+
+def bench_ours(args):
+    import torch
+
+    from paper_2310_01801_b200.workloads import config1
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    w = config1(seed=1 + rank)
+    T = args.T
+    qd, kd, vd, cd, qh, kh, vh, clsh = make_inputs(w, dev)
+    slopes = torch.tensor(w.slopes, dtype=torch.float32, device=dev)
+    sinks = torch.tensor(w.sinks, dtype=torch.float32, device=dev)
+    N, D = w.N, w.D
+    dec = ([qd[:, :, N + t] for t in range(D)], [kd[:, :, N + t] for t in range(D)],
+           [vd[:, :, N + t] for t in range(D)], [cd[:, N + t].contiguous() for t in range(D)])
+
+    # untimed: live counts per step (for the algorithmic byte count)
+    res, cache, lives = run_session(w, T, qd, kd, vd, cd, slopes, sinks, dec, record=True)
+    cache.check()
+    bytes_per_launch = decode_bytes(w, res, lives)
+    kept0 = int(res.kept_count.sum())
+    pruned = 1.0 - float(lives[-1].sum()) / float(w.B * w.H * (N + D))
+    del cache
+
+    for _ in range(args.warmup):
+        run_session(w, T, qd, kd, vd, cd, slopes, sinks, dec)
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_wall = time.perf_counter()
+        for s in range(args.steps):
+            run_session(w, T, qd, kd, vd, cd, slopes, sinks, dec, ev=evs[s])
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
+    if dist is not None:
+        dist.barrier()
+    enc_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    dec_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    tot_ms = float(evs[0][0].elapsed_time(evs[-1][2]))
+    if dist is not None:
+        t = torch.tensor([tot_ms, max(enc_ms), max(dec_ms)], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms, enc_max, dec_max = t.tolist()
+    ms_per_step = tot_ms / args.steps
+    tokens = w.B * D * args.steps * world
+    value = tokens / (tot_ms / 1e3)
+    dec_avg_ms = statistics.mean(dec_ms)
+    launch_us = dec_avg_ms * 1e3 / D
+    avg_bytes = statistics.mean(bytes_per_launch)
+    achieved = avg_bytes / (launch_us * 1e-6) / 1e9
+    peaks, peak_kind = _peaks()
+
+    # sweep over the config's other thresholds (1 warm + 1 timed session each)
+    sweep = {}
+    for Ts in w.thresholds:
+        run_session(w, Ts, qd, kd, vd, cd, slopes, sinks, dec)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        r2, c2, _ = run_session(w, Ts, qd, kd, vd, cd, slopes, sinks, dec, ev=e)
+        torch.cuda.synchronize()
+        fam = r2.family
+        pol = np.bincount(r2.choice[:, 0], minlength=len(fam))
+        sweep[f"{Ts:g}"] = {
+            "tok_s": w.B * D / (e[0].elapsed_time(e[2]) / 1e3),
+            "profiling_ms": e[0].elapsed_time(e[1]),
+            "decode_ms": e[1].elapsed_time(e[2]),
+            "final_cache_tokens": c2.total_retained(),
+            "pruned_ratio": 1.0 - c2.total_retained() / float(w.B * w.H * (N + D)),
+            "policies": {str(fam[i]): int(pol[i]) for i in range(len(fam)) if pol[i]},
+        }
+
+    e2e = bench_e2e(w, T, args, qh, kh, vh, clsh, slopes, sinks, dev, dist)
+
+    if rank != 0:
+        return
+    line = {
+        "metric": "decode tok/s with adaptive KV at fixed T (session incl. profiling)",
+        "value": value,
+        "unit": "tok/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (seeded N(0,1) Q/K/V, planted local/sink heads; see DESIGN.md)",
+        "config": {
+            "workload": f"c1 Llama-7B-shape layer: B={w.B} H={w.H} d={w.d} N={N} D={D} bf16, T={T:g}",
+            "parallelism": f"dp{world} (independent batches per GPU)",
+            "step": "one session: K1 profile + K2 compact + D K3 decode steps",
+            "l2": "inputs larger than L2: every decode step streams the ~130-200 MB arena (L2 126 MB)",
+        },
+        "profiling_ms_per_layer": statistics.mean(enc_ms),
+        "decode_only_tok_s": w.B * D / (dec_avg_ms / 1e3),
+        "decode_us_per_step": launch_us,
+        "kept_tokens_after_profile": kept0,
+        "pruned_ratio_end": pruned,
+        "sweep": sweep,
+        "gpu_launches": args.steps * (5 + D),
+        "roofline": {
+            "kernel": "k3_decode (akv_decode_step)",
+            "bound": "hbm",
+            "achieved": achieved,
+            "peak": peaks.get("hbm_gbs"),
+            "peak_kind": peak_kind,
+            "unit": "GB/s",
+            "frac": achieved / peaks.get("hbm_gbs"),
+            "traffic": None,
+            "algorithmic_bytes_per_launch": avg_bytes,
+            "avg_launch_us": launch_us,
+        },
+        "clocks": clk.summary(),
+        "wall_s": t_wall,
+        "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_port(w, T)
+    print(json.dumps(line), flush=True)
+
+
+def bench_e2e(w, T, args, qh, kh, vh, clsh, slopes, sinks, dev, dist):
+    """Same sessions through the public API from pinned HOST buffers: H2D of
+    the prompt and of every decode token's rows, D2H of every step's output,
+    all inside the timed region."""
+    import torch
+
+    from paper_2310_01801_b200 import ProfilerConfig, decode_step_tensors, encode_prompt_tensors
+
+    N, D = w.N, w.D
+    dt = torch.bfloat16 if w.dtype == "bf16" else torch.float32
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dt).pin_memory()
+    hq, hk, hv = pin(qh[:, :, :N]), pin(kh[:, :, :N]), pin(vh[:, :, :N])
+    hc = torch.from_numpy(np.ascontiguousarray(clsh[:, :N])).pin_memory()
+    sq = pin(np.moveaxis(qh[:, :, N:], 2, 0))   # [D, B, H, d]
+    sk = pin(np.moveaxis(kh[:, :, N:], 2, 0))
+    sv = pin(np.moveaxis(vh[:, :, N:], 2, 0))
+    sc = torch.from_numpy(np.ascontiguousarray(clsh[:, N:].T)).pin_memory()  # [D, B]
+    hout = torch.empty(D, w.B, w.H, w.d, dtype=torch.float32).pin_memory()
+    cfg = ProfilerConfig(recovery_threshold=T)
+    bq = torch.empty(w.B, w.H, w.d, dtype=dt, device=dev)
+    bk, bv = torch.empty_like(bq), torch.empty_like(bq)
+    bc = torch.empty(w.B, dtype=torch.uint8, device=dev)
+
+    def session():
+        q = hq.to(dev, non_blocking=True)
+        k = hk.to(dev, non_blocking=True)
+        v = hv.to(dev, non_blocking=True)
+        c = hc.to(dev, non_blocking=True)
+        _, cache = encode_prompt_tensors(q, k, v, c, cfg, max_new_tokens=D, slopes=slopes,
+                                         sinks=sinks)
+        for t in range(D):
+            bq.copy_(sq[t], non_blocking=True)
+            bk.copy_(sk[t], non_blocking=True)
+            bv.copy_(sv[t], non_blocking=True)
+            bc.copy_(sc[t], non_blocking=True)
+            o = decode_step_tensors(cache, bq, bk, bv, bc)
+            hout[t].copy_(o, non_blocking=True)
+        return cache
+
+    for _ in range(max(1, args.warmup)):
+        session()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        session()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    world = 1
+    if dist is not None:
+        world = dist.get_world_size()
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    es = 2 if w.dtype == "bf16" else 4
+    h2d = 3 * w.B * w.H * N * w.d * es + w.B * N + D * (3 * w.B * w.H * w.d * es + w.B)
+    d2h = D * w.B * w.H * w.d * 4
+    return {"value": world * w.B * D * args.steps / (ms / 1e3), "unit": "tok/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (the oracle port: tests/bench are the only importers of oracle/)
+
+def _oracle_heads(args):
+    """Run the oracle session for a set of heads of one batch row; returns
+    seconds spent (inputs generated before the clock starts)."""
+    w_seed, b, heads, T, B, H, N, D = args
+    from oracle import akv_oracle as O
+    from paper_2310_01801_b200.workloads import class_lut, config1
+
+    w = config1(seed=w_seed, B=B, H=H, N=N, D=D)
+    cls = class_lut()[w.tokens(b)].astype(np.int64)
+    data = [tuple(x.astype(np.float64) for x in w.head_qkv(b, h)) for h in heads]
+    fam = O.default_family(w.r_l, w.r_f)
+    t0 = time.perf_counter()
+    for h, (q, k, v) in zip(heads, data):
+        prof = O.profile_head(q[:N], k[:N], v[:N], cls, w.slopes[h], w.sinks[h], fam, [T])
+        st = O.compact_head(prof, k[:N], v[:N], fam[prof.choice[0]], N, w.slopes[h], w.sinks[h])
+        for t in range(D):
+            O.decode_head(st, q[N + t], k[N + t], v[N + t], N + t, cls, N)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline_port(w, T):
+    """Oracle port on one host core over a bounded sample: batch row 0 of the
+    workload, 8 of its 32 heads (2 planted + 6 plain), full session."""
+    planted = [h for h in range(w.H) if w.slopes[h] or w.sinks[h]][:2]
+    plain = [h for h in range(w.H) if h not in planted][:6]
+    heads = planted + plain
+    secs = _oracle_heads((w.seed, 0, heads, T, w.B, w.H, w.N, w.D))
+    # heads of a row are independent: a full row costs H/len(heads) times more
+    row_secs = secs * w.H / len(heads)
+    return {"value": w.D / row_secs, "unit": "tok/s", "cores": 1, "kind": "port",
+            "sample": f"oracle (float64 numpy port of the reference) on batch row 0, "
+                      f"{len(heads)} of {w.H} heads, N={w.N}, D={w.D}, T={T:g}; "
+                      "scaled to the full row (heads are independent)"}
+
+
+def bench_reference(args):
+    """--impl reference: the reference algorithm on the host cores (the
+    oracle port; the Python reference itself is not on the GPU box).  Each
+    step = one full session of one batch row (32 heads, N=1024, D=512),
+    heads spread over a process pool using every available core."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    from paper_2310_01801_b200.workloads import config1
+
+    w = config1(seed=1)
+    T = args.T
+    cores = len(os.sched_getaffinity(0))
+    workers = max(1, min(cores, w.H))
+    chunks = [list(range(w.H))[i::workers] for i in range(workers)]
+    jobs = [(w.seed, 0, c, T, w.B, w.H, w.N, w.D) for c in chunks]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(workers) as pool:
+        for _ in range(args.warmup):
+            pool.map(_oracle_heads, jobs)
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            pool.map(_oracle_heads, jobs)
+            times.append(time.perf_counter() - t0)
+    step_s = statistics.mean(times)
+    value = w.D / step_s
+    print(json.dumps({
+        "impl": "reference",
+        "metric": "decode tok/s with adaptive KV at fixed T (session incl. profiling)",
+        "value": value, "unit": "tok/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (same seeded workload as the GPU arm)",
+        "config": {"workload": f"c1 Llama-7B-shape layer: B={w.B} H={w.H} d={w.d} N={w.N} "
+                               f"D={w.D}, T={T:g}; one batch row per step",
+                   "parallelism": f"{workers} host processes over heads"},
+        "cpu_baseline": {"value": value, "unit": "tok/s", "cores": workers, "kind": "port",
+                         "sample": "batch row 0 (32 heads) full session per step"},
+        "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--T", type=float, default=0.95)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_ours(args)
+
+
+if __name__ == "__main__":
+    main()

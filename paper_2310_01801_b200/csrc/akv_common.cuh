@@ -9,11 +9,29 @@
 
 namespace akv {
 
-constexpr int kClsShift = 24;          // meta = position | class << 24
+constexpr int kClsShift = 24;          // meta = position | class << 24 | inF << 30
 constexpr int kPosMask = (1 << kClsShift) - 1;
+constexpr int kInF = 1 << 30;          // slot is in the frequent top-k set
 
 __device__ __forceinline__ int meta_pos(int m) { return m & kPosMask; }
-__device__ __forceinline__ int meta_cls(int m) { return (m >> kClsShift) & 0xff; }
+__device__ __forceinline__ int meta_cls(int m) { return (m >> kClsShift) & 0x3f; }
+
+// Thread-group synchronisation policies for the block-level helpers: the
+// whole CTA (barrier 0) or a named barrier over a warp-aligned subset.
+struct BlockSync {
+  static constexpr int kThreads = 0;  // dynamic (blockDim.x)
+  __device__ __forceinline__ static void sync() { __syncthreads(); }
+  __device__ __forceinline__ static int tid() { return threadIdx.x; }
+  __device__ __forceinline__ static int nthreads() { return blockDim.x; }
+};
+template <int NT, int ID, int FIRST>
+struct NamedSync {
+  static constexpr int kThreads = NT;
+  static constexpr int kWarps = NT / 32;
+  __device__ __forceinline__ static void sync() { asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(NT) : "memory"); }
+  __device__ __forceinline__ static int tid() { return threadIdx.x - FIRST; }
+  __device__ __forceinline__ static int nthreads() { return NT; }
+};
 
 // policies.py:205-206: max(1, ceil(r*L - 1e-9)) in IEEE float64, with the
 // product and the subtraction rounded separately (no FMA contraction), so
@@ -80,43 +98,44 @@ __device__ __forceinline__ int warp_sum_i(int v) {
   return v;
 }
 
-// Block-wide sum (deterministic tree order); `red` needs blockDim/32 slots.
-template <typename V>
+// Group-wide sum (deterministic tree order); `red` needs nthreads/32 slots.
+template <typename V, typename Sync = BlockSync>
 __device__ __forceinline__ V block_sum(V v, V* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = Sync::tid() & 31, warp = Sync::tid() >> 5, nw = Sync::nthreads() >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __syncthreads();
+  Sync::sync();
   if (lane == 0) red[warp] = v;
-  __syncthreads();
+  Sync::sync();
   V t = V(0);
   for (int i = 0; i < nw; ++i) t += red[i];
-  __syncthreads();
+  Sync::sync();
   return t;
 }
 
-// Exclusive block scan of small ints; returns the exclusive prefix of this
-// thread and writes the block total to *total.  `red` needs blockDim/32+1.
+// Exclusive group scan of small ints; returns the exclusive prefix of this
+// thread and writes the group total to *total.  `red` needs nthreads/32+1.
+template <typename Sync = BlockSync>
 __device__ __forceinline__ int block_exclusive_scan(int v, int* red, int* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = Sync::tid() & 31, warp = Sync::tid() >> 5, nw = Sync::nthreads() >> 5;
   int x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     int y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
-  __syncthreads();
+  Sync::sync();
   if (lane == 31) red[warp] = x;
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  Sync::sync();
+  if (Sync::tid() == 0) {
     int acc = 0;
     for (int i = 0; i < nw; ++i) { int t = red[i]; red[i] = acc; acc += t; }
     red[nw] = acc;
   }
-  __syncthreads();
+  Sync::sync();
   int ex = red[warp] + x - v;
   *total = red[nw];
-  __syncthreads();
+  Sync::sync();
   return ex;
 }
 
@@ -134,9 +153,10 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* red, int* total)
 // top-k iff key > thr_key || (key == thr_key && pos <= thr_pos).  If k >= n
 // everything is selected (thr_key = 0, thr_pos = INT_MAX).
 // `hist` needs 256 ints of shared memory, `red` 33 ints.
-template <typename Get>
+template <typename Sync = BlockSync, typename Get>
 __device__ void block_topk_threshold(int n, int k, Get get, int* hist, int* red,
                                      unsigned long long* thr_key, int* thr_pos) {
+  const int tid = Sync::tid(), nth = Sync::nthreads();
   if (k >= n) {
     *thr_key = 0ull;
     *thr_pos = 0x7fffffff;
@@ -144,22 +164,22 @@ __device__ void block_topk_threshold(int n, int k, Get get, int* hist, int* red,
   }
   __shared__ unsigned long long s_prefix;
   __shared__ int s_remain, s_digit;
-  if (threadIdx.x == 0) { s_prefix = 0ull; s_remain = k; }
-  __syncthreads();
+  if (tid == 0) { s_prefix = 0ull; s_remain = k; }
+  Sync::sync();
   unsigned long long mask = 0ull;
   for (int shift = 56; shift >= 0; shift -= 8) {
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
+    for (int i = tid; i < 256; i += nth) hist[i] = 0;
+    Sync::sync();
     const unsigned long long prefix = s_prefix;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    for (int i = tid; i < n; i += nth) {
       unsigned long long key; int pos;
       get(i, &key, &pos);
       if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 0xff], 1);
     }
-    __syncthreads();
-    if (threadIdx.x < 32) {
+    Sync::sync();
+    if (tid < 32) {
       // suffix scan over 256 bins (descending digit): lane owns 8 bins
-      const int lane = threadIdx.x;
+      const int lane = tid;
       int c[8], s = 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j) { c[j] = hist[255 - (lane * 8 + j)]; s += c[j]; }
@@ -188,25 +208,25 @@ __device__ void block_topk_threshold(int n, int k, Get get, int* hist, int* red,
         s_prefix = prefix | ((unsigned long long)dg << shift);
       }
     }
-    __syncthreads();
+    Sync::sync();
     mask |= (0xffull << shift);
   }
   const unsigned long long vstar = s_prefix;
   const int need_eq = s_remain;  // how many elements equal to v* are selected (>= 1)
   // count elements equal to v*
   int cnt = 0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+  for (int i = tid; i < n; i += nth) {
     unsigned long long key; int pos;
     get(i, &key, &pos);
     cnt += (key == vstar);
   }
   cnt = warp_sum_i(cnt);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
-  __syncthreads();
+  Sync::sync();
+  if ((tid & 31) == 0) red[tid >> 5] = cnt;
+  Sync::sync();
   int n_eq = 0;
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) n_eq += red[i];
-  __syncthreads();
+  for (int i = 0; i < (nth >> 5); ++i) n_eq += red[i];
+  Sync::sync();
   if (n_eq == need_eq) {
     *thr_key = vstar;
     *thr_pos = 0x7fffffff;
@@ -215,21 +235,21 @@ __device__ void block_topk_threshold(int n, int k, Get get, int* hist, int* red,
   // ties: select the need_eq smallest positions among key == v* (radix on
   // inverted 24-bit positions, largest inverted == smallest position).
   __shared__ int s_pprefix, s_premain;
-  if (threadIdx.x == 0) { s_pprefix = 0; s_premain = need_eq; }
-  __syncthreads();
+  if (tid == 0) { s_pprefix = 0; s_premain = need_eq; }
+  Sync::sync();
   int pmask = 0;
   for (int shift = 16; shift >= 0; shift -= 8) {
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
+    for (int i = tid; i < 256; i += nth) hist[i] = 0;
+    Sync::sync();
     const int prefix = s_pprefix;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    for (int i = tid; i < n; i += nth) {
       unsigned long long key; int pos;
       get(i, &key, &pos);
       int ip = kPosMask - pos;
       if (key == vstar && (ip & pmask) == prefix) atomicAdd(&hist[(ip >> shift) & 0xff], 1);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    Sync::sync();
+    if (tid == 0) {
       int remain = s_premain, run = 0;
       for (int dg = 255; dg >= 0; --dg) {
         if (run + hist[dg] >= remain) {
@@ -240,7 +260,7 @@ __device__ void block_topk_threshold(int n, int k, Get get, int* hist, int* red,
         run += hist[dg];
       }
     }
-    __syncthreads();
+    Sync::sync();
     pmask |= (0xff << shift);
   }
   *thr_key = vstar;
@@ -250,6 +270,107 @@ __device__ void block_topk_threshold(int n, int k, Get get, int* hist, int* red,
 __device__ __forceinline__ bool topk_selected(unsigned long long key, int pos,
                                               unsigned long long thr_key, int thr_pos) {
   return key > thr_key || (key == thr_key && pos <= thr_pos);
+}
+
+}  // namespace akv
+
+namespace akv {
+
+// Register-resident variant of block_topk_threshold: thread t holds up to
+// EPT candidates in key[]/pos[] (the first `cnt` are valid).  Same result
+// contract (threshold (key, pos) of the k-th largest under (key desc, pos
+// asc)); every pass is a shared-memory histogram over registers.
+template <typename Sync, int EPT>
+__device__ void regs_topk_threshold(int n, int k, const unsigned long long* key, const int* pos,
+                                    int cnt, int* hist, unsigned long long* thr_key, int* thr_pos) {
+  const int tid = Sync::tid(), nth = Sync::nthreads();
+  if (k >= n) {
+    *thr_key = 0ull;
+    *thr_pos = 0x7fffffff;
+    return;
+  }
+  __shared__ unsigned long long s_prefix;
+  __shared__ int s_remain, s_neq;
+  if (tid == 0) { s_prefix = 0ull; s_remain = k; s_neq = 0; }
+  Sync::sync();
+  unsigned long long mask = 0ull;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = tid; i < 256; i += nth) hist[i] = 0;
+    Sync::sync();
+    const unsigned long long prefix = s_prefix;
+#pragma unroll
+    for (int i = 0; i < EPT; ++i)
+      if (i < cnt && (key[i] & mask) == prefix) atomicAdd(&hist[(key[i] >> shift) & 0xff], 1);
+    Sync::sync();
+    if (tid < 32) {
+      const int lane = tid;
+      int c[8], s = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { c[j] = hist[255 - (lane * 8 + j)]; s += c[j]; }
+      int incl = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int remain = s_remain;
+      int found = -1, above = 0, run = incl - s;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (found < 0 && run < remain && run + c[j] >= remain) { found = 255 - (lane * 8 + j); above = run; }
+        run += c[j];
+      }
+      const unsigned ball = __ballot_sync(0xffffffffu, found >= 0);
+      const int src = __ffs(ball) - 1;
+      const int dg = __shfl_sync(0xffffffffu, found, src);
+      const int ab = __shfl_sync(0xffffffffu, above, src);
+      if (lane == 0) {
+        s_remain = remain - ab;
+        s_prefix = prefix | ((unsigned long long)dg << shift);
+      }
+    }
+    Sync::sync();
+    mask |= (0xffull << shift);
+  }
+  const unsigned long long vstar = s_prefix;
+  const int need_eq = s_remain;
+  int mine = 0;
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) mine += (i < cnt && key[i] == vstar);
+  if (mine) atomicAdd(&s_neq, mine);
+  Sync::sync();
+  if (s_neq == need_eq) {
+    *thr_key = vstar;
+    *thr_pos = 0x7fffffff;
+    return;
+  }
+  // ties on the value: the need_eq smallest positions win (inverted-position radix)
+  __shared__ int s_pp, s_pr;
+  if (tid == 0) { s_pp = 0; s_pr = need_eq; }
+  Sync::sync();
+  int pmask = 0;
+  for (int shift = 16; shift >= 0; shift -= 8) {
+    for (int i = tid; i < 256; i += nth) hist[i] = 0;
+    Sync::sync();
+    const int prefix = s_pp;
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int ip = kPosMask - pos[i];
+      if (i < cnt && key[i] == vstar && (ip & pmask) == prefix) atomicAdd(&hist[(ip >> shift) & 0xff], 1);
+    }
+    Sync::sync();
+    if (tid == 0) {
+      int remain = s_pr, run = 0;
+      for (int dg = 255; dg >= 0; --dg) {
+        if (run + hist[dg] >= remain) { s_pr = remain - run; s_pp = prefix | (dg << shift); break; }
+        run += hist[dg];
+      }
+    }
+    Sync::sync();
+    pmask |= (0xff << shift);
+  }
+  *thr_key = vstar;
+  *thr_pos = kPosMask - s_pp;
 }
 
 }  // namespace akv

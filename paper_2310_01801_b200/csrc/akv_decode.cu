@@ -10,47 +10,55 @@
 //   current_len = pos+1 (policies.py:214-267, engine.py:332-338)
 //   drop the rows it no longer keeps (evicted rows never return).
 //
-// Layout: each head g owns arena slots [seg_off[g], seg_off[g]+seg_cap[g]);
-// slots [0, live) are live rows (any order), row = d elements of K (kc) and
-// V (vc), meta = position | class<<24, score = float64 cumulative attention.
+// Layout: head g owns arena slots [seg_off[g], seg_off[g]+seg_cap[g]);
+// slots [0, live) hold live rows (any order): d elements of K (kc) and V
+// (vc), meta = position | class<<24 | inF<<30, score = float64 cumulative
+// attention (FREQUENT heads).
 //
-// One launch = one step for all B*H heads.  grid = (max chunks, B*H); CTA
-// (c, g) streams C consecutive slots of head g with 16-byte non-allocating
-// loads (all of the chunk's K and V rows are in flight before the first
-// FMA), computes logits, a chunk-local softmax and the PV partial, and
-// publishes (max, sum, o[d]) to the workspace.  The last CTA of a head to
-// finish (split-K semaphore) combines the partials, writes the output and
-// runs the policy epilogue: score update, keep rule (exact top-k on
-// (score desc, position asc)), and swap-remove compaction of evicted rows
-// (only the few evicted holes are filled, from the segment tail).  The
-// chunk that holds slot `live` reads the new row from the inputs and
-// stores it into the cache (fused insert).  live_in/live_out are distinct
-// buffers so CTAs that exit early never see this step's update.
+// Kernel structure (one launch per step for all heads): a persistent grid
+// of 2 CTAs per SM.  The step's work is cut into 16 KB "pages" of K and V
+// (64 slots of bf16 d=128); every CTA computes the per-head page counts
+// from live_in and takes one contiguous, equal share of the flattened page
+// list.  The last warp is the producer: one elected lane streams each
+// page's K rows, V rows, slot metadata and the head's q (plus the new
+// token's k/v for the page holding slot `live`) into a 3-stage shared
+// memory ring (TMA, mbarrier transaction counts).  The other warps consume:
+// logits with the planted bias, online softmax, PV accumulation per head
+// segment; at the end of a head's segment they publish (max, sum, o[d])
+// and bump the head's split-K semaphore.  The CTA completing a head runs
+// its epilogue while its producer keeps prefetching: combine, output,
+// score update, keep rule (exact top-k on (score desc, position asc) with
+// an incremental fast path and a radix-select fallback) and swap-remove
+// compaction of the evicted rows.  The consumer owning slot `live` writes
+// the new token's row into the arena (fused insert).  live_in / live_out
+// are distinct buffers (double-buffered across steps).
+//
+// Two consumers share this skeleton:
+//  * bf16, d in {64,128} (the production path): pages arrive through 2-D
+//    TMA with the 128-byte swizzle, and each consumer warp turns a
+//    16-key x 16-dim tile into logits and PV with bf16 mma.sync
+//    (ldmatrix / ldmatrix.trans, fp32 accumulate), so the SIMT pipes only
+//    run the softmax.  Logits (and hence scores) stay fp32; p is rounded to
+//    bf16 for the PV product (the cache itself is bf16).
+//  * everything else (fp32 caches, small head dims): 1-D bulk copies and
+//    SIMT dot products, 8 consumer warps.
 
 #include <math.h>
 
 #include "akv_common.cuh"
 #include "akv_internal.h"
+#include "akv_tma.cuh"
 
 namespace akv {
 
-constexpr int kDecWarps = 4;
-constexpr int kDecSteps = 8;  // row steps per warp per chunk
-
-template <typename T, int D>
-struct DecShape {
-  static constexpr int EV = Elem<T>::kPerVec;  // elements per 16-byte vector
-  static constexpr int LPR = D / EV;           // lanes per row
-  static constexpr int RPW = 32 / LPR;         // rows per warp step
-  static constexpr int C = kDecSteps * kDecWarps * RPW;  // slots per chunk
-  static_assert(LPR >= 1 && LPR <= 32 && (32 % LPR) == 0, "unsupported head dim");
-};
-
-// smallest chunk over dtypes for a head dim (sizes the workspace)
-static inline int min_chunk(int d) { return kDecSteps * kDecWarps * (32 / (d * 4 / 16)); }
+constexpr int kStages = 3;
+constexpr int kPageBytes = 16384;  // per K (and per V) page
+constexpr int kMaxHeads = 2048;
+constexpr int kEpt = 16;
+constexpr int kSmemEvict = 64;  // evictions per head-step paired through shared memory  // register-resident candidates per thread in the epilogue
 
 struct DecParams {
-  int B, H, prompt_len, pos;
+  int B, H, G, prompt_len, pos;
   const void* q;
   const void* kn;
   const void* vn;
@@ -72,275 +80,1177 @@ struct DecParams {
   float* out;
   int32_t* evicted;
   int32_t* status;
-  float* part;       // [G, max_chunks, D+2]
+  float* part;       // [G, max_parts, D+2]
   float* logit;      // [total_slots]
   int32_t* counter;  // [G]
-  int max_chunks;
+  int max_parts;
   float scale;
+  unsigned long long* trace;  // optional [grid, 8] globaltimer stamps (AKV_DEC_TRACE)
 };
 
-template <typename T, int D>
-__global__ void __launch_bounds__(kDecWarps * 32) k3_decode(DecParams p) {
-  using S = DecShape<T, D>;
-  constexpr int EV = S::EV, LPR = S::LPR, RPW = S::RPW, C = S::C;
-  constexpr int RV = D * sizeof(T) / 16;  // 16-byte vectors per row (== LPR)
-  __shared__ float s_red[kDecWarps][D];
-  __shared__ float s_m[kDecWarps], s_l[kDecWarps];
-  __shared__ int s_last;
-  __shared__ int hist[256];
-  __shared__ int red_i[33];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define AKV_TRACE(slot)                                                        \
+  do {                                                                          \
+    if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 8 + (slot)] = gtimer(); \
+  } while (0)
 
-  const int g = blockIdx.y, c = blockIdx.x;
-  const int L = p.live_in[g];
-  const int n = L + 1;
-  const int start = c * C;
-  if (L < 0 || start >= n) return;
-  if (n > p.seg_cap[g]) {  // capacity: every CTA of the head agrees and bails
-    if (c == 0 && threadIdx.x == 0) atomicExch(p.status, AKV_ERR_CAPACITY);
-    return;
-  }
-  const int nchunks = (n + C - 1) / C;
-  const int b = g / p.H, h = g % p.H;
-  const int64_t base = p.seg_off[g];
-  const uint8_t atoms = p.atoms[g];
-  const bool freq = (atoms & AKV_ATOM_FREQUENT) && !(atoms & AKV_ATOM_FULL);
-  const int posq = p.pos;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int sub = lane / LPR, sl = lane % LPR;
-  const float slope = p.slope ? p.slope[h] : 0.f;
-  const float sink = p.sink ? p.sink[h] : 0.f;
-  const int new_cls = p.new_cls[b];
+// owner CTA of flattened page pg when P pages are split evenly over `grid`
+// (CTA i owns [floor(i*P/grid), floor((i+1)*P/grid)))
+__device__ __forceinline__ int page_owner(long long pg, long long P, int grid) {
+  return (int)(((pg + 1) * grid - 1) / P);
+}
 
-  const uint4* kc = static_cast<const uint4*>(p.kc) + base * RV;
-  const uint4* vc = static_cast<const uint4*>(p.vc) + base * RV;
-  const uint4* kn = reinterpret_cast<const uint4*>(static_cast<const T*>(p.kn) + (size_t)g * p.bh_stride);
-  const uint4* vn = reinterpret_cast<const uint4*>(static_cast<const T*>(p.vn) + (size_t)g * p.bh_stride);
-  const uint4* qv = reinterpret_cast<const uint4*>(static_cast<const T*>(p.q) + (size_t)g * p.bh_stride);
+struct HeadCtx {
+  int g, L, n;
+  int64_t base;
+  uint8_t atoms;
+  bool freq;
+  float slope, sink;
+  int ncls;
+};
 
-  // issue every K/V load of the chunk before using any of them
-  uint4 kr[kDecSteps], vr[kDecSteps];
-  int mt[kDecSteps];
-#pragma unroll
-  for (int s = 0; s < kDecSteps; ++s) {
-    const int slot = start + (s * kDecWarps + warp) * RPW + sub;
-    if (slot < L) {
-      kr[s] = ld_nc_v4(kc + (size_t)slot * RV + sl);
-      vr[s] = ld_nc_v4(vc + (size_t)slot * RV + sl);
-      mt[s] = p.meta[base + slot];
-    } else if (slot == L) {  // fused insert of the new token
-      kr[s] = kn[sl];
-      vr[s] = vn[sl];
-      mt[s] = posq | (new_cls << kClsShift);
-      uint4* kw = static_cast<uint4*>(p.kc) + (base + slot) * RV;
-      uint4* vw = static_cast<uint4*>(p.vc) + (base + slot) * RV;
-      st_v4(kw + sl, kr[s]);
-      st_v4(vw + sl, vr[s]);
-      if (sl == 0) {
-        p.meta[base + slot] = mt[s];
-        p.score[base + slot] = 0.0;  // policies.py:357
-      }
-    } else {
-      kr[s] = make_uint4(0, 0, 0, 0);
-      vr[s] = make_uint4(0, 0, 0, 0);
-      mt[s] = -1;
+__device__ __forceinline__ void load_head(const DecParams& p, int g, int L, HeadCtx& hc) {
+  hc.g = g;
+  hc.L = L;
+  hc.n = L + 1;
+  hc.base = p.seg_off[g];
+  hc.atoms = p.atoms[g];
+  hc.freq = (hc.atoms & AKV_ATOM_FREQUENT) && !(hc.atoms & AKV_ATOM_FULL);
+  const int h = g % p.H;
+  hc.slope = p.slope ? p.slope[h] : 0.f;
+  hc.sink = p.sink ? p.sink[h] : 0.f;
+  hc.ncls = p.new_cls[g / p.H];
+}
+
+__device__ __forceinline__ float biased_logit(float dot, int mt, const HeadCtx& hc, int pos) {
+  float x = dot;
+  if (meta_cls(mt) == AKV_CLS_SPECIAL) x += hc.sink;
+  if (hc.slope != 0.f) x -= hc.slope * (float)(pos - meta_pos(mt));
+  return x;
+}
+
+// ---------------------------------------------------------------------------
+// Page plan, run by every CTA: pages per head from live_in and their
+// exclusive prefix in shared memory.  Heads whose segment cannot take the
+// new row are skipped and flagged (capacity error).
+__device__ __forceinline__ long long plan_pages(const DecParams& p, int page, int* s_prefix,
+                                                int* s_live, int* red_i) {
+  const int G = p.G;
+  const int per = (G + blockDim.x - 1) / blockDim.x;
+  const int lo = min(G, (int)threadIdx.x * per), hi = min(G, lo + per);
+  int cnt = 0;
+  for (int g = lo; g < hi; ++g) {
+    const int L = p.live_in[g];
+    int np = 0;
+    if (L >= 0 && L + 1 <= p.seg_cap[g]) {
+      np = (L + 1 + page - 1) / page;
+    } else if (L >= 0 && blockIdx.x == 0) {
+      atomicExch(p.status, AKV_ERR_CAPACITY);
+      p.live_out[g] = L;
     }
+    s_live[g] = np > 0 ? L : -1;
+    cnt += np;
   }
-  float qf[EV];
-  Elem<T>::unpack(qv[sl], qf);
-#pragma unroll
-  for (int e = 0; e < EV; ++e) qf[e] *= p.scale;
+  int total;
+  int off = block_exclusive_scan<BlockSync>(cnt, red_i, &total);
+  for (int g = lo; g < hi; ++g) {
+    s_prefix[g] = off;
+    off += s_live[g] >= 0 ? (s_live[g] + 1 + page - 1) / page : 0;
+  }
+  if (threadIdx.x == 0) s_prefix[G] = total;
+  __syncthreads();
+  return s_prefix[G];
+}
 
-  // logits (engine.py:95) + planted head bias
-  float sj[kDecSteps];
-  float mx = -INFINITY;
-#pragma unroll
-  for (int s = 0; s < kDecSteps; ++s) {
-    float kf[EV];
-    Elem<T>::unpack(kr[s], kf);
-    float dot = 0.f;
-#pragma unroll
-    for (int e = 0; e < EV; ++e) dot = fmaf(qf[e], kf[e], dot);
-#pragma unroll
-    for (int o = 1; o < LPR; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-    float x = -INFINITY;
-    if (mt[s] >= 0) {
-      x = dot;
-      if (meta_cls(mt[s]) == AKV_CLS_SPECIAL) x += sink;
-      if (slope != 0.f) x -= slope * (float)(posq - meta_pos(mt[s]));
-    }
-    sj[s] = x;
-    mx = fmaxf(mx, x);
+// largest g with s_prefix[g] <= pg
+__device__ __forceinline__ int head_of_page(const int* s_prefix, int G, long long pg) {
+  int lo = 0, hi = G - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (s_prefix[mid] <= pg) lo = mid; else hi = mid - 1;
   }
-  if (freq && sl == 0) {
-#pragma unroll
-    for (int s = 0; s < kDecSteps; ++s) {
-      const int slot = start + (s * kDecWarps + warp) * RPW + sub;
-      if (slot < L) p.logit[base + slot] = sj[s];
-    }
-  }
-  mx = warp_allreduce(mx, [](float a, float b) { return fmaxf(a, b); });
-  if (lane == 0) s_m[warp] = mx;
-  __syncthreads();
-  float M = s_m[0];
-#pragma unroll
-  for (int w = 1; w < kDecWarps; ++w) M = fmaxf(M, s_m[w]);
+  return lo;
+}
 
-  // chunk-local softmax numerator and PV partial
-  float o[EV];
-#pragma unroll
-  for (int e = 0; e < EV; ++e) o[e] = 0.f;
-  float lsum = 0.f;
-#pragma unroll
-  for (int s = 0; s < kDecSteps; ++s) {
-    const float pe = (sj[s] == -INFINITY) ? 0.f : __expf(sj[s] - M);
-    if (sl == 0) lsum += pe;
-    float vf[EV];
-    Elem<T>::unpack(vr[s], vf);
-#pragma unroll
-    for (int e = 0; e < EV; ++e) o[e] = fmaf(pe, vf[e], o[e]);
-  }
-  // reduce over the RPW rows of a warp step (lanes with equal sl)
-#pragma unroll
-  for (int off = LPR; off < 32; off <<= 1) {
-#pragma unroll
-    for (int e = 0; e < EV; ++e) o[e] += __shfl_xor_sync(0xffffffffu, o[e], off);
-  }
-  lsum = warp_allreduce(lsum, [](float a, float b) { return a + b; });
-  if (sub == 0) {
-#pragma unroll
-    for (int e = 0; e < EV; ++e) s_red[warp][sl * EV + e] = o[e];
-  }
-  if (lane == 0) s_l[warp] = lsum;
-  __syncthreads();
-  float* part = p.part + ((size_t)g * p.max_chunks + c) * (D + 2);
-  for (int t = threadIdx.x; t < D; t += blockDim.x) {
-    float acc = 0.f;
-#pragma unroll
-    for (int w = 0; w < kDecWarps; ++w) acc += s_red[w][t];
-    part[t] = acc;
-  }
-  if (threadIdx.x == 0) {
-    float l = 0.f;
-#pragma unroll
-    for (int w = 0; w < kDecWarps; ++w) l += s_l[w];
-    part[D] = M;
-    part[D + 1] = l;
-  }
-  // split-K semaphore: the last CTA of this head runs the epilogue
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(&p.counter[g], 1) == nchunks - 1);
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-
-  // ---- epilogue (one CTA per head) ----
-  const float* parts = p.part + (size_t)g * p.max_chunks * (D + 2);
-  float gM = -INFINITY;
-  for (int k = 0; k < nchunks; ++k) gM = fmaxf(gM, __ldcg(parts + (size_t)k * (D + 2) + D));
-  float gl = 0.f;
-  for (int k = 0; k < nchunks; ++k) {
-    const float* pk = parts + (size_t)k * (D + 2);
-    gl += __ldcg(pk + D + 1) * __expf(__ldcg(pk + D) - gM);
-  }
-  const float inv = 1.f / gl;
-  for (int t = threadIdx.x; t < D; t += blockDim.x) {
-    float acc = 0.f;
-    for (int k = 0; k < nchunks; ++k) {
-      const float* pk = parts + (size_t)k * (D + 2);
-      acc += __ldcg(pk + t) * __expf(__ldcg(pk + D) - gM);
-    }
-    p.out[(size_t)g * D + t] = acc * inv;
-  }
-  if (atoms & AKV_ATOM_FULL) {  // full cache: nothing is ever evicted
-    if (threadIdx.x == 0) {
-      p.live_out[g] = n;
-      if (p.evicted) p.evicted[g] = 0;
-      p.counter[g] = 0;
-    }
-    return;
-  }
-  const float lse = gM + logf(gl);
-  const int cur = posq + 1;
-  double* score = p.score + base;
-  const int32_t* meta = p.meta + base;
-  if (freq) {  // engine.py:320-330 / policies.py:355-357 (score[new] is 0)
-    const float* lg = p.logit + base;
-    for (int j = threadIdx.x; j < L; j += blockDim.x)
-      score[j] += (double)expf(__ldcg(lg + j) - lse);
-  }
-  __syncthreads();
-  unsigned long long thr_key = 0ull;
-  int thr_pos = 0x7fffffff;
+// Keep rule + compaction for heads with more than NC*kEpt candidates:
+// every pass streams the head's slot metadata from L2.
+template <typename CS>
+__device__ void policy_global(const DecParams& p, const HeadCtx& hc, float lse, int* hist,
+                              int* red_i, int rv) {
+  constexpr int NC = CS::kThreads, NW = CS::kWarps;
+  const int tid = CS::tid(), lane = tid & 31, warp = tid >> 5;
+  const int g = hc.g, L = hc.L, n = hc.n;
+  const int cur = p.pos + 1;
+  double* score = p.score + hc.base;
+  int32_t* meta = p.meta + hc.base;
+  const uint8_t atoms = hc.atoms;
+  const bool freq = hc.freq;
+  __shared__ int s_fast;
+  __shared__ int s_add;  // slot joining the frequent set on the fast path (-1: none)
+  __shared__ unsigned long long s_k[2][NW];
+  __shared__ int s_i[4][NW];
   if (freq) {
-    const int kb = budget(p.r_f[g], cur);
-    auto get = [&](int i, unsigned long long* key, int* pos) {
-      *key = (unsigned long long)__double_as_longlong(__ldcg(score + i));
-      *pos = meta_pos(__ldcg(meta + i));
-    };
-    block_topk_threshold(n, kb, get, hist, red_i, &thr_key, &thr_pos);
+    // score update (policies.py:355-357; score[new] = 0 was written by the
+    // inserting consumer) fused with the fast-path statistics: the smallest
+    // key of the current frequent set F and the largest key outside it.
+    const float* lg = p.logit + hc.base;
+    unsigned long long minF_k = ~0ull, maxN_k = 0ull;
+    int minF_p = -1, maxN_p = 0x7fffffff, maxN_slot = -1, cntF = 0, anyN = 0;
+    for (int j = tid; j < n; j += NC) {
+      double s = __ldcg(score + j);
+      if (j < L) {
+        s += (double)expf(__ldcg(lg + j) - lse);
+        score[j] = s;
+      }
+      const int m = __ldcg(meta + j);
+      const unsigned long long key = (unsigned long long)__double_as_longlong(s);
+      const int ps = meta_pos(m);
+      if (m & kInF) {
+        ++cntF;
+        if (key < minF_k || (key == minF_k && ps > minF_p)) { minF_k = key; minF_p = ps; }
+      } else if (!anyN || key > maxN_k || (key == maxN_k && ps < maxN_p)) {
+        maxN_k = key; maxN_p = ps; maxN_slot = j; anyN = 1;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, minF_k, o);
+      const int op = __shfl_xor_sync(0xffffffffu, minF_p, o);
+      if (ok < minF_k || (ok == minF_k && op > minF_p)) { minF_k = ok; minF_p = op; }
+      const unsigned long long nk = __shfl_xor_sync(0xffffffffu, maxN_k, o);
+      const int np_ = __shfl_xor_sync(0xffffffffu, maxN_p, o);
+      const int ns = __shfl_xor_sync(0xffffffffu, maxN_slot, o);
+      const int na = __shfl_xor_sync(0xffffffffu, anyN, o);
+      if (na && (!anyN || nk > maxN_k || (nk == maxN_k && np_ < maxN_p))) {
+        maxN_k = nk; maxN_p = np_; maxN_slot = ns; anyN = 1;
+      }
+      cntF += __shfl_xor_sync(0xffffffffu, cntF, o);
+    }
+    CS::sync();
+    if (lane == 0) {
+      s_k[0][warp] = minF_k; s_i[0][warp] = minF_p;
+      s_k[1][warp] = maxN_k; s_i[1][warp] = maxN_p;
+      s_i[2][warp] = anyN ? maxN_slot : -1;
+      s_i[3][warp] = cntF;
+    }
+    CS::sync();
+    if (tid == 0) {
+      unsigned long long mf = ~0ull, mn = 0ull;
+      int mfp = -1, mnp = 0x7fffffff, mns = -1, cf = 0;
+      bool an = false;
+      for (int w = 0; w < NW; ++w) {
+        cf += s_i[3][w];
+        if (s_k[0][w] < mf || (s_k[0][w] == mf && s_i[0][w] > mfp)) { mf = s_k[0][w]; mfp = s_i[0][w]; }
+        if (s_i[2][w] >= 0 && (!an || s_k[1][w] > mn || (s_k[1][w] == mn && s_i[1][w] < mnp))) {
+          mn = s_k[1][w]; mnp = s_i[1][w]; mns = s_i[2][w]; an = true;
+        }
+      }
+      const int kb = budget(p.r_f[g], cur);
+      int f = 0, add = -1;
+      if (kb >= n) {
+        f = 2;  // every candidate is selected
+      } else if (cf > 0 && (kb == cf || kb == cf + 1)) {
+        // F is still the top-|F| set iff all of F outranks everything else
+        const bool separated = !an || mn < mf || (mn == mf && mnp > mfp);
+        if (separated) {
+          f = 1;
+          if (kb == cf + 1) add = mns;
+        }
+      }
+      s_fast = f;
+      s_add = add;
+    }
+    CS::sync();
+    if (s_fast == 1) {
+      if (tid == 0 && s_add >= 0) meta[s_add] = __ldcg(meta + s_add) | kInF;
+    } else {
+      unsigned long long thr_key = 0ull;
+      int thr_pos = 0x7fffffff;
+      if (s_fast == 0) {
+        if (p.trace && tid == 0) atomicAdd(&p.trace[blockIdx.x * 8 + 7], 1ull);  // fallbacks
+        const int kb = budget(p.r_f[g], cur);
+        auto get = [&](int i, unsigned long long* key, int* pos) {
+          *key = (unsigned long long)__double_as_longlong(__ldcg(score + i));
+          *pos = meta_pos(__ldcg(meta + i));
+        };
+        block_topk_threshold<CS>(n, kb, get, hist, red_i, &thr_key, &thr_pos);
+      }
+      CS::sync();
+      // rewrite the inF flags from the exact threshold
+      for (int j = tid; j < n; j += NC) {
+        const int m = __ldcg(meta + j);
+        const bool sel = topk_selected((unsigned long long)__double_as_longlong(__ldcg(score + j)),
+                                       meta_pos(m), thr_key, thr_pos);
+        const int nm = sel ? (m | kInF) : (m & ~kInF);
+        if (nm != m) meta[j] = nm;
+      }
+    }
+    CS::sync();
   }
   const int window_start = cur - budget(p.r_l[g], p.prompt_len);
   auto keep = [&](int j) -> bool {
     const int m = __ldcg(meta + j);
     const int cl = meta_cls(m), ps = meta_pos(m);
-    bool k = ((atoms & AKV_ATOM_SPECIAL) && cl == AKV_CLS_SPECIAL) ||
-             ((atoms & AKV_ATOM_PUNCT) && cl == AKV_CLS_PUNCT) ||
-             ((atoms & AKV_ATOM_LOCAL) && ps >= window_start);
-    if (freq && !k)
-      k = topk_selected((unsigned long long)__double_as_longlong(__ldcg(score + j)), ps, thr_key, thr_pos);
-    return k;
+    return ((atoms & AKV_ATOM_SPECIAL) && cl == AKV_CLS_SPECIAL) ||
+           ((atoms & AKV_ATOM_PUNCT) && cl == AKV_CLS_PUNCT) ||
+           ((atoms & AKV_ATOM_LOCAL) && ps >= window_start) || (freq && (m & kInF));
   };
   // count kept, then pair holes (evicted slots below n') with donors (kept
   // slots at or above n'), both in slot order
-  const int per = (n + blockDim.x - 1) / blockDim.x;
-  const int lo = min(n, (int)threadIdx.x * per), hi = min(n, lo + per);
+  const int per = (n + NC - 1) / NC;
+  const int lo = min(n, tid * per), hi = min(n, lo + per);
   int nk = 0;
   for (int j = lo; j < hi; ++j) nk += keep(j);
-  const int n_keep = block_sum(nk, red_i);
-  int holes = 0, donors = 0;
-  for (int j = lo; j < hi; ++j) {
-    const bool k = keep(j);
-    holes += (j < n_keep && !k);
-    donors += (j >= n_keep && k);
-  }
-  int n_holes, n_donors;
-  int hole_off = block_exclusive_scan(holes, red_i, &n_holes);
-  int donor_off = block_exclusive_scan(donors, red_i, &n_donors);
-  int* hole_list = reinterpret_cast<int*>(p.logit + base);  // logits are consumed
-  int* donor_list = hole_list + n_holes;
-  __syncthreads();
-  for (int j = lo; j < hi; ++j) {
-    const bool k = keep(j);
-    if (j < n_keep && !k) hole_list[hole_off++] = j;
-    if (j >= n_keep && k) donor_list[donor_off++] = j;
-  }
-  __syncthreads();
-  uint4* kw = static_cast<uint4*>(p.kc) + base * RV;
-  uint4* vw = static_cast<uint4*>(p.vc) + base * RV;
-  for (int r = warp; r < n_holes; r += kDecWarps) {
-    const int dst = hole_list[r], src = donor_list[r];
-    for (int v = lane; v < RV; v += 32) {
-      st_v4(kw + (size_t)dst * RV + v, ld_cg_v4(kw + (size_t)src * RV + v));
-      st_v4(vw + (size_t)dst * RV + v, ld_cg_v4(vw + (size_t)src * RV + v));
+  const int n_keep = block_sum<int, CS>(nk, red_i);
+  if (n_keep < n) {
+    int holes = 0, donors = 0;
+    for (int j = lo; j < hi; ++j) {
+      const bool k = keep(j);
+      holes += (j < n_keep && !k);
+      donors += (j >= n_keep && k);
     }
-    if (lane == 0) {
-      p.meta[base + dst] = __ldcg(meta + src);
-      score[dst] = __ldcg(score + src);
+    int n_holes, n_donors;
+    int hole_off = block_exclusive_scan<CS>(holes, red_i, &n_holes);
+    int donor_off = block_exclusive_scan<CS>(donors, red_i, &n_donors);
+    int* hole_list = reinterpret_cast<int*>(p.logit + hc.base);  // logits are consumed
+    int* donor_list = hole_list + n_holes;
+    for (int j = lo; j < hi; ++j) {
+      const bool k = keep(j);
+      if (j < n_keep && !k) hole_list[hole_off++] = j;
+      if (j >= n_keep && k) donor_list[donor_off++] = j;
+    }
+    CS::sync();
+    uint4* kw = static_cast<uint4*>(p.kc) + hc.base * rv;
+    uint4* vw = static_cast<uint4*>(p.vc) + hc.base * rv;
+    for (int r = warp; r < n_holes; r += NW) {
+      const int dst = __ldcg(hole_list + r), src = __ldcg(donor_list + r);
+      for (int v = lane; v < rv; v += 32) {
+        st_v4(kw + (size_t)dst * rv + v, ld_cg_v4(kw + (size_t)src * rv + v));
+        st_v4(vw + (size_t)dst * rv + v, ld_cg_v4(vw + (size_t)src * rv + v));
+      }
+      if (lane == 0) {
+        meta[dst] = __ldcg(meta + src);
+        score[dst] = __ldcg(score + src);
+      }
     }
   }
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     p.live_out[g] = n_keep;
     if (p.evicted) p.evicted[g] = n - n_keep;
     p.counter[g] = 0;
   }
+  CS::sync();
+}
+
+
+// Keep rule + compaction with each thread's contiguous slice of the
+// candidates (<= kEpt) held in registers: one load pass, then reductions
+// and scans on registers, one write-back pass.
+template <typename CS>
+__device__ void policy_regs(const DecParams& p, const HeadCtx& hc, float lse, int* hist,
+                            int* red_i, int rv) {
+  constexpr int NC = CS::kThreads, NW = CS::kWarps;
+  const int tid = CS::tid(), lane = tid & 31, warp = tid >> 5;
+  const int g = hc.g, L = hc.L, n = hc.n;
+  const int cur = p.pos + 1;
+  double* score = p.score + hc.base;
+  int32_t* meta = p.meta + hc.base;
+  const uint8_t atoms = hc.atoms;
+  const bool freq = hc.freq;
+  const int per = (n + NC - 1) / NC;
+  const int lo = min(n, tid * per), hi = min(n, lo + per);
+  int mt[kEpt];
+  double sc[kEpt];
+#pragma unroll
+  for (int i = 0; i < kEpt; ++i) {
+    const int j = lo + i;
+    mt[i] = (j < hi) ? __ldcg(meta + j) : 0;
+    sc[i] = (freq && j < hi) ? __ldcg(score + j) : 0.0;
+  }
+  __shared__ int s_fast, s_add;
+  __shared__ unsigned long long s_k[2][NW];
+  __shared__ int s_i[4][NW];
+  if (freq) {
+    // score update (policies.py:355-357; score[new] = 0 was written by the
+    // inserting consumer) and the fast-path statistics: the smallest key of
+    // the current frequent set F and the largest key outside it
+    const float* lg = p.logit + hc.base;
+    float lv[kEpt];
+#pragma unroll
+    for (int i = 0; i < kEpt; ++i) lv[i] = (lo + i < hi && lo + i < L) ? __ldcg(lg + lo + i) : 0.f;
+    unsigned long long minF_k = ~0ull, maxN_k = 0ull;
+    int minF_p = -1, maxN_p = 0x7fffffff, maxN_slot = -1, cntF = 0, anyN = 0;
+#pragma unroll
+    for (int i = 0; i < kEpt; ++i) {
+      const int j = lo + i;
+      if (j >= hi) continue;
+      if (j < L) {
+        sc[i] += (double)expf(lv[i] - lse);
+        score[j] = sc[i];
+      }
+      const unsigned long long key = (unsigned long long)__double_as_longlong(sc[i]);
+      const int ps = meta_pos(mt[i]);
+      if (mt[i] & kInF) {
+        ++cntF;
+        if (key < minF_k || (key == minF_k && ps > minF_p)) { minF_k = key; minF_p = ps; }
+      } else if (!anyN || key > maxN_k || (key == maxN_k && ps < maxN_p)) {
+        maxN_k = key; maxN_p = ps; maxN_slot = j; anyN = 1;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, minF_k, o);
+      const int op = __shfl_xor_sync(0xffffffffu, minF_p, o);
+      if (ok < minF_k || (ok == minF_k && op > minF_p)) { minF_k = ok; minF_p = op; }
+      const unsigned long long nk = __shfl_xor_sync(0xffffffffu, maxN_k, o);
+      const int np_ = __shfl_xor_sync(0xffffffffu, maxN_p, o);
+      const int ns = __shfl_xor_sync(0xffffffffu, maxN_slot, o);
+      const int na = __shfl_xor_sync(0xffffffffu, anyN, o);
+      if (na && (!anyN || nk > maxN_k || (nk == maxN_k && np_ < maxN_p))) {
+        maxN_k = nk; maxN_p = np_; maxN_slot = ns; anyN = 1;
+      }
+      cntF += __shfl_xor_sync(0xffffffffu, cntF, o);
+    }
+    CS::sync();
+    if (lane == 0) {
+      s_k[0][warp] = minF_k; s_i[0][warp] = minF_p;
+      s_k[1][warp] = maxN_k; s_i[1][warp] = maxN_p;
+      s_i[2][warp] = anyN ? maxN_slot : -1;
+      s_i[3][warp] = cntF;
+    }
+    CS::sync();
+    if (tid == 0) {
+      unsigned long long mf = ~0ull, mn = 0ull;
+      int mfp = -1, mnp = 0x7fffffff, mns = -1, cf = 0;
+      bool an = false;
+      for (int w = 0; w < NW; ++w) {
+        cf += s_i[3][w];
+        if (s_k[0][w] < mf || (s_k[0][w] == mf && s_i[0][w] > mfp)) { mf = s_k[0][w]; mfp = s_i[0][w]; }
+        if (s_i[2][w] >= 0 && (!an || s_k[1][w] > mn || (s_k[1][w] == mn && s_i[1][w] < mnp))) {
+          mn = s_k[1][w]; mnp = s_i[1][w]; mns = s_i[2][w]; an = true;
+        }
+      }
+      const int kb = budget(p.r_f[g], cur);
+      int f = 0, add = -1;
+      if (kb >= n) {
+        f = 2;  // every candidate is selected
+      } else if (cf > 0 && (kb == cf || kb == cf + 1)) {
+        // F is still the top-|F| set iff all of F outranks everything else
+        const bool separated = !an || mn < mf || (mn == mf && mnp > mfp);
+        if (separated) {
+          f = 1;
+          if (kb == cf + 1) add = mns;
+        }
+      }
+      s_fast = f;
+      s_add = add;
+    }
+    CS::sync();
+    const int fast = s_fast, add = s_add;
+    unsigned long long thr_key = 0ull;
+    int thr_pos = 0x7fffffff;
+    if (fast == 0) {  // exact radix select over the registers (rare)
+      if (p.trace && tid == 0) atomicAdd(&p.trace[blockIdx.x * 8 + 7], 1ull);
+      unsigned long long kk[kEpt];
+      int pp[kEpt];
+#pragma unroll
+      for (int i = 0; i < kEpt; ++i) {
+        kk[i] = (unsigned long long)__double_as_longlong(sc[i]);
+        pp[i] = meta_pos(mt[i]);
+      }
+      regs_topk_threshold<CS, kEpt>(n, budget(p.r_f[g], cur), kk, pp, hi - lo, hist, &thr_key,
+                                    &thr_pos);
+    }
+#pragma unroll
+    for (int i = 0; i < kEpt; ++i) {
+      const int j = lo + i;
+      if (j >= hi) continue;
+      int nm = mt[i];
+      if (fast == 1) {
+        if (j == add) nm |= kInF;
+      } else {
+        const bool sel = topk_selected((unsigned long long)__double_as_longlong(sc[i]),
+                                       meta_pos(mt[i]), thr_key, thr_pos);
+        nm = sel ? (nm | kInF) : (nm & ~kInF);
+      }
+      if (nm != mt[i]) { mt[i] = nm; meta[j] = nm; }
+    }
+  }
+  const int window_start = cur - budget(p.r_l[g], p.prompt_len);
+  bool kp[kEpt];
+  int nk = 0;
+#pragma unroll
+  for (int i = 0; i < kEpt; ++i) {
+    const int cl = meta_cls(mt[i]), ps = meta_pos(mt[i]);
+    kp[i] = (lo + i < hi) &&
+            (((atoms & AKV_ATOM_SPECIAL) && cl == AKV_CLS_SPECIAL) ||
+             ((atoms & AKV_ATOM_PUNCT) && cl == AKV_CLS_PUNCT) ||
+             ((atoms & AKV_ATOM_LOCAL) && ps >= window_start) || (freq && (mt[i] & kInF)));
+    nk += kp[i];
+  }
+  const int n_keep = block_sum<int, CS>(nk, red_i);
+  if (n_keep < n) {
+    int holes = 0, donors = 0;
+#pragma unroll
+    for (int i = 0; i < kEpt; ++i) {
+      const int j = lo + i;
+      if (j >= hi) continue;
+      holes += (j < n_keep && !kp[i]);
+      donors += (j >= n_keep && kp[i]);
+    }
+    int n_holes, n_donors;
+    int hole_off = block_exclusive_scan<CS>(holes, red_i, &n_holes);
+    int donor_off = block_exclusive_scan<CS>(donors, red_i, &n_donors);
+    // pairing lists: shared memory for the usual handful of evictions,
+    // the (consumed) logit scratch of the head otherwise
+    __shared__ int s_lists[2 * kSmemEvict];
+    int* hole_list = n_holes <= kSmemEvict ? s_lists : reinterpret_cast<int*>(p.logit + hc.base);
+    int* donor_list = n_holes <= kSmemEvict ? s_lists + kSmemEvict : hole_list + n_holes;
+#pragma unroll
+    for (int i = 0; i < kEpt; ++i) {
+      const int j = lo + i;
+      if (j >= hi) continue;
+      if (j < n_keep && !kp[i]) hole_list[hole_off++] = j;
+      if (j >= n_keep && kp[i]) donor_list[donor_off++] = j;
+    }
+    CS::sync();
+    uint4* kw = static_cast<uint4*>(p.kc) + hc.base * rv;
+    uint4* vw = static_cast<uint4*>(p.vc) + hc.base * rv;
+    for (int r = warp; r < n_holes; r += NW) {
+      const int dst = n_holes <= kSmemEvict ? hole_list[r] : __ldcg(hole_list + r);
+      const int src = n_holes <= kSmemEvict ? donor_list[r] : __ldcg(donor_list + r);
+      for (int v = lane; v < rv; v += 32) {
+        st_v4(kw + (size_t)dst * rv + v, ld_cg_v4(kw + (size_t)src * rv + v));
+        st_v4(vw + (size_t)dst * rv + v, ld_cg_v4(vw + (size_t)src * rv + v));
+      }
+      if (lane == 0) {
+        meta[dst] = __ldcg(meta + src);
+        score[dst] = __ldcg(score + src);
+      }
+    }
+  }
+  if (tid == 0) {
+    p.live_out[g] = n_keep;
+    if (p.evicted) p.evicted[g] = n - n_keep;
+    p.counter[g] = 0;
+  }
+  CS::sync();
+}
+
+// ---------------------------------------------------------------------------
+// Epilogue of one head (consumer warps only, named barrier 1).
+template <typename CS, int D>
+__device__ void head_epilogue(const DecParams& p, const HeadCtx& hc, int nparts, int rv,
+                              int* hist, int* red_i) {
+  constexpr int NC = CS::kThreads, NW = CS::kWarps;
+  const int tid = CS::tid(), lane = tid & 31, warp = tid >> 5;
+  const int g = hc.g, L = hc.L, n = hc.n;
+  // combine the partials of all contributing CTAs; every thread issues its
+  // loads for a batch of parts (max, sum and its output dims) at once, so a
+  // batch costs one L2 round trip
+  const float* parts = p.part + (size_t)g * p.max_parts * (D + 2);
+  constexpr int kB = 8;
+  constexpr int DPT = (D + NC - 1) / NC;  // output dims per thread
+  float gM = -INFINITY, gl = 0.f, acc[DPT];
+#pragma unroll
+  for (int u = 0; u < DPT; ++u) acc[u] = 0.f;
+  for (int k0 = 0; k0 < nparts; k0 += kB) {
+    float mk[kB], lk[kB], ok[kB][DPT];
+#pragma unroll
+    for (int b = 0; b < kB; ++b) {
+      const bool v = k0 + b < nparts;
+      const float* pk = parts + (size_t)(k0 + b) * (D + 2);
+      mk[b] = v ? __ldcg(pk + D) : -INFINITY;
+      lk[b] = v ? __ldcg(pk + D + 1) : 0.f;
+#pragma unroll
+      for (int u = 0; u < DPT; ++u) {
+        const int t = tid + u * NC;
+        ok[b][u] = (v && t < D) ? __ldcg(pk + t) : 0.f;
+      }
+    }
+    float newM = gM;
+#pragma unroll
+    for (int b = 0; b < kB; ++b) newM = fmaxf(newM, mk[b]);
+    const float rs = (gM == -INFINITY) ? 0.f : __expf(gM - newM);
+    gl *= rs;
+#pragma unroll
+    for (int u = 0; u < DPT; ++u) acc[u] *= rs;
+#pragma unroll
+    for (int b = 0; b < kB; ++b) {
+      const float w = (mk[b] == -INFINITY) ? 0.f : __expf(mk[b] - newM);
+      gl += w * lk[b];
+#pragma unroll
+      for (int u = 0; u < DPT; ++u) acc[u] += w * ok[b][u];
+    }
+    gM = newM;
+  }
+  {
+    const float inv = 1.f / gl;
+#pragma unroll
+    for (int u = 0; u < DPT; ++u) {
+      const int t = tid + u * NC;
+      if (t < D) p.out[(size_t)g * D + t] = acc[u] * inv;
+    }
+  }
+  if (hc.atoms & AKV_ATOM_FULL) {  // the full cache never evicts
+    if (tid == 0) {
+      p.live_out[g] = n;
+      if (p.evicted) p.evicted[g] = 0;
+      p.counter[g] = 0;
+    }
+    CS::sync();
+    return;
+  }
+  const float lse = gM + logf(gl);
+  if ((n + NC - 1) / NC <= kEpt)
+    policy_regs<CS>(p, hc, lse, hist, red_i, rv);
+  else
+    policy_global<CS>(p, hc, lse, hist, red_i, rv);
+}
+
+// Publish a CTA's partial (max, sum, o[D]) for head g from NWC per-warp
+// values in s_red / s_ml (group CS), bump the semaphore, and run the
+// epilogue if this CTA is the last contributor.  `release` (optional) is
+// arrived on once s_red / s_ml have been consumed.
+template <typename CS, int NWC, int D>
+__device__ __forceinline__ void publish_head(const DecParams& p, const HeadCtx& hc,
+                                             const int* s_prefix, long long P, int grid,
+                                             const float (*s_red)[D], const float (*s_ml)[2],
+                                             int* s_last, int rv, int* hist, int* red_i,
+                                             uint64_t* release) {
+  constexpr int NC = CS::kThreads;
+  const int tid = CS::tid();
+  const int g = hc.g;
+  CS::sync();
+  const int own0 = page_owner(s_prefix[g], P, grid);
+  const int nparts = page_owner(s_prefix[g + 1] - 1, P, grid) - own0 + 1;
+  float* part = p.part + ((size_t)g * p.max_parts + (blockIdx.x - own0)) * (D + 2);
+  float M = -INFINITY;
+#pragma unroll
+  for (int w = 0; w < NWC; ++w) M = fmaxf(M, s_ml[w][0]);
+  for (int t = tid; t < D; t += NC) {
+    float acc = 0.f;
+#pragma unroll
+    for (int w = 0; w < NWC; ++w)
+      if (s_ml[w][0] != -INFINITY) acc += s_red[w][t] * __expf(s_ml[w][0] - M);
+    part[t] = acc;
+  }
+  if (tid == 0) {
+    float l = 0.f;
+#pragma unroll
+    for (int w = 0; w < NWC; ++w)
+      if (s_ml[w][0] != -INFINITY) l += s_ml[w][1] * __expf(s_ml[w][0] - M);
+    part[D] = M;
+    part[D + 1] = l;
+  }
+  CS::sync();  // the partial is written by the whole group ...
+  if (tid == 0) {  // ... and released to the device by one thread (cumulative)
+    if (release) mbar_arrive(release);
+    int prev;
+    asm volatile("fence.acq_rel.gpu;\n\tatom.add.acq_rel.gpu.global.s32 %0, [%1], 1;"
+                 : "=r"(prev) : "l"(p.counter + g) : "memory");
+    *s_last = (prev == nparts - 1);
+  }
+  CS::sync();
+  if (*s_last) head_epilogue<CS, D>(p, hc, nparts, rv, hist, red_i);
+}
+
+// ===========================================================================
+// SIMT consumer (fp32 caches, any supported head dim): 1-D bulk copies.
+template <typename T, int D>
+struct SimtShape {
+  static constexpr int NW = 8;
+  static constexpr int EV = Elem<T>::kPerVec;
+  static constexpr int RB = D * (int)sizeof(T);
+  static constexpr int LPR = RB / 16;
+  static constexpr int RPW = 32 / LPR;
+  static constexpr int PAGE = kPageBytes / RB;
+  static constexpr int STEPS = PAGE / (NW * RPW);
+  static constexpr int META_B = PAGE * 4;
+  static constexpr int STAGE_B = 2 * kPageBytes + META_B + 3 * RB;
+  static_assert(LPR >= 1 && LPR <= 32 && (32 % LPR) == 0, "unsupported head dim");
+  static_assert(STEPS >= 1 && STEPS * NW * RPW == PAGE, "page split");
+};
+
+template <typename T, int D>
+__global__ void __launch_bounds__(SimtShape<T, D>::NW * 32 + 32, 2) k3_decode_simt(DecParams p) {
+  using S = SimtShape<T, D>;
+  constexpr int NW = S::NW, EV = S::EV, RB = S::RB, LPR = S::LPR, RPW = S::RPW, PAGE = S::PAGE;
+  constexpr int STEPS = S::STEPS;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
+  __shared__ float s_red[NW][D];
+  __shared__ float s_ml[NW][2];
+  __shared__ int s_last;
+  __shared__ int hist[256];
+  __shared__ int red_i[33];
+
+  const int G = p.G;
+  int* s_prefix = reinterpret_cast<int*>(smem + kStages * S::STAGE_B);
+  int* s_live = s_prefix + (G + 1);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], NW); }
+    mbar_fence_init();
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const long long P = plan_pages(p, PAGE, s_prefix, s_live, red_i);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int grid = (int)(P < (long long)gridDim.x ? P : (long long)gridDim.x);
+  if ((int)blockIdx.x >= grid) return;
+  const long long pbeg = (long long)blockIdx.x * P / grid;
+  const long long pend = (long long)(blockIdx.x + 1) * P / grid;
+  const int g0 = head_of_page(s_prefix, G, pbeg);
+
+  if (warp == NW) {  // ---------------- producer ----------------
+    if (lane == 0) {
+      const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
+      int g = g0, stage = 0;
+      uint32_t phase = 0;
+      for (long long pg = pbeg; pg < pend; ++pg) {
+        while (pg >= s_prefix[g + 1]) ++g;
+        const int L = s_live[g];
+        const int slot0 = (int)(pg - s_prefix[g]) * PAGE;
+        const int rows = max(0, min(PAGE, L - slot0));
+        const bool has_new = (L >= slot0 && L < slot0 + PAGE);
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* st = smem + stage * S::STAGE_B;
+        const int64_t base = p.seg_off[g];
+        const uint32_t meta_b = ((rows * 4) + 15) & ~15;
+        const uint32_t bytes = 2u * rows * RB + (rows ? meta_b : 0) + RB + (has_new ? 2 * RB : 0);
+        mbar_arrive_expect_tx(&full_bar[stage], bytes);
+        if (rows) {
+          bulk_g2s(st, static_cast<const uint8_t*>(p.kc) + (base + slot0) * RB, rows * RB,
+                   &full_bar[stage], pol_stream);
+          bulk_g2s(st + kPageBytes, static_cast<const uint8_t*>(p.vc) + (base + slot0) * RB,
+                   rows * RB, &full_bar[stage], pol_stream);
+          bulk_g2s(st + 2 * kPageBytes, p.meta + base + slot0, meta_b, &full_bar[stage], pol_keep);
+        }
+        uint8_t* hdr = st + 2 * kPageBytes + S::META_B;
+        bulk_g2s(hdr, static_cast<const T*>(p.q) + (size_t)g * p.bh_stride, RB, &full_bar[stage],
+                 pol_keep);
+        if (has_new) {
+          bulk_g2s(hdr + RB, static_cast<const T*>(p.kn) + (size_t)g * p.bh_stride, RB,
+                   &full_bar[stage], pol_keep);
+          bulk_g2s(hdr + 2 * RB, static_cast<const T*>(p.vn) + (size_t)g * p.bh_stride, RB,
+                   &full_bar[stage], pol_keep);
+        }
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int sub = lane / LPR, sl = lane % LPR;
+  int g = g0, stage = 0;
+  uint32_t phase = 0;
+  HeadCtx hc;
+  hc.g = -1;
+  float m_run = -INFINITY, l_run = 0.f;
+  float o[EV];
+#pragma unroll
+  for (int e = 0; e < EV; ++e) o[e] = 0.f;
+
+  for (long long pg = pbeg; pg < pend; ++pg) {
+    while (pg >= s_prefix[g + 1]) ++g;
+    if (g != hc.g) load_head(p, g, s_live[g], hc);
+    const int L = hc.L;
+    const int slot0 = (int)(pg - s_prefix[g]) * PAGE;
+    mbar_wait(&full_bar[stage], phase);
+    const uint8_t* st = smem + stage * S::STAGE_B;
+    const uint4* kpage = reinterpret_cast<const uint4*>(st);
+    const uint4* vpage = reinterpret_cast<const uint4*>(st + kPageBytes);
+    const int* mpage = reinterpret_cast<const int*>(st + 2 * kPageBytes);
+    const uint4* hdr = reinterpret_cast<const uint4*>(st + 2 * kPageBytes + S::META_B);
+    float qf[EV];
+    Elem<T>::unpack(hdr[sl], qf);
+#pragma unroll
+    for (int e = 0; e < EV; ++e) qf[e] *= p.scale;
+    float sj[STEPS];
+    float pm = -INFINITY;
+#pragma unroll
+    for (int s = 0; s < STEPS; ++s) {
+      const int row = warp * (PAGE / NW) + s * RPW + sub;
+      const int slot = slot0 + row;
+      uint4 kv;
+      int mt;
+      if (slot < L) { kv = kpage[row * LPR + sl]; mt = mpage[row]; }
+      else if (slot == L) { kv = hdr[LPR + sl]; mt = p.pos | (hc.ncls << kClsShift); }
+      else { kv = make_uint4(0, 0, 0, 0); mt = -1; }
+      float kf[EV];
+      Elem<T>::unpack(kv, kf);
+      float dot = 0.f;
+#pragma unroll
+      for (int e = 0; e < EV; ++e) dot = fmaf(qf[e], kf[e], dot);
+#pragma unroll
+      for (int off = 1; off < LPR; off <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+      float x = -INFINITY;
+      if (mt >= 0) {
+        x = biased_logit(dot, mt, hc, p.pos);
+        if (hc.freq && sl == 0 && slot < L) p.logit[hc.base + slot] = x;
+      }
+      sj[s] = x;
+      pm = fmaxf(pm, x);
+    }
+    pm = warp_allreduce(pm, [](float a, float b) { return fmaxf(a, b); });
+    const float m_new = fmaxf(m_run, pm);
+    if (m_new != -INFINITY) {
+      const float sc = (m_run == -INFINITY) ? 0.f : __expf(m_run - m_new);
+      l_run *= sc;
+#pragma unroll
+      for (int e = 0; e < EV; ++e) o[e] *= sc;
+#pragma unroll
+      for (int s = 0; s < STEPS; ++s) {
+        const int row = warp * (PAGE / NW) + s * RPW + sub;
+        const int slot = slot0 + row;
+        const float pe = (sj[s] == -INFINITY) ? 0.f : __expf(sj[s] - m_new);
+        if (sl == 0) l_run += pe;
+        uint4 vv;
+        if (slot < L) vv = vpage[row * LPR + sl];
+        else if (slot == L) vv = hdr[2 * LPR + sl];
+        else vv = make_uint4(0, 0, 0, 0);
+        float vf[EV];
+        Elem<T>::unpack(vv, vf);
+#pragma unroll
+        for (int e = 0; e < EV; ++e) o[e] = fmaf(pe, vf[e], o[e]);
+        if (slot == L) {  // fused insert of the new token's row
+          uint4* kw = static_cast<uint4*>(p.kc) + (hc.base + slot) * LPR;
+          uint4* vw = static_cast<uint4*>(p.vc) + (hc.base + slot) * LPR;
+          st_v4(kw + sl, hdr[LPR + sl]);
+          st_v4(vw + sl, vv);
+          if (sl == 0) {
+            p.meta[hc.base + slot] = p.pos | (hc.ncls << kClsShift);
+            p.score[hc.base + slot] = 0.0;  // policies.py:357
+          }
+        }
+      }
+      m_run = m_new;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[stage]);
+    if (++stage == kStages) { stage = 0; phase ^= 1; }
+
+    if (!((pg + 1 == pend) || (pg + 1 == s_prefix[g + 1]))) continue;
+#pragma unroll
+    for (int off = LPR; off < 32; off <<= 1) {
+#pragma unroll
+      for (int e = 0; e < EV; ++e) o[e] += __shfl_xor_sync(0xffffffffu, o[e], off);
+    }
+    l_run = warp_allreduce(l_run, [](float a, float b) { return a + b; });
+    if (sub == 0) {
+#pragma unroll
+      for (int e = 0; e < EV; ++e) s_red[warp][sl * EV + e] = o[e];
+    }
+    if (lane == 0) { s_ml[warp][0] = m_run; s_ml[warp][1] = l_run; }
+    publish_head<NamedSync<NW * 32, 1, 0>, NW, D>(p, hc, s_prefix, P, grid, s_red, s_ml, &s_last,
+                                                  LPR, hist, red_i, nullptr);
+    m_run = -INFINITY;
+    l_run = 0.f;
+#pragma unroll
+    for (int e = 0; e < EV; ++e) o[e] = 0.f;
+  }
+}
+
+// ===========================================================================
+// bf16 tensor-core consumer (d = 64 / 128): 2-D TMA with the 128-byte
+// swizzle, ldmatrix + mma.sync.m16n8k16 (bf16 in, fp32 accumulate).
+template <int D>
+struct MmaShape {
+  static constexpr int NW = 4;                      // consumer warps
+  static constexpr int NE = 4;                      // epilogue warps
+  static constexpr int THREADS = (NW + 1 + NE) * 32; // + producer warp
+  static constexpr int EFIRST = (NW + 1) * 32;      // first epilogue thread
+  static constexpr int RB = D * 2;
+  static constexpr int PAGE = kPageBytes / RB;      // 64 (d=128) / 128 (d=64)
+  static constexpr int KPW = PAGE / NW;             // keys per warp per page
+  static constexpr int TILES = KPW / 16;            // 16-key tiles per warp
+  static constexpr int NBOX = D / 64;               // 64-column TMA boxes per page
+  static constexpr int BOX_B = PAGE * 128;          // bytes per box
+  static constexpr int META_B = PAGE * 4;
+  static constexpr int HDR_OFF = 2 * kPageBytes + META_B;
+  static constexpr int STAGE_B = ((HDR_OFF + 3 * RB) + 1023) & ~1023;  // 1 KB aligned stages
+  static_assert(TILES >= 1 && KPW % 16 == 0, "page split");
+};
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2,
+                                        uint32_t& a3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2,
+                                          uint32_t& a3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float* c, uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// byte offset of (row r, 16-byte chunk c of the d axis) in a swizzled page
+template <int D>
+__device__ __forceinline__ uint32_t swz(int r, int c) {
+  return (uint32_t)((c >> 3) * MmaShape<D>::BOX_B + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+}
+
+// Consumer -> epilogue handoff of one head segment's per-warp results.
+template <int NW, int D>
+struct PubSlot {
+  float red[NW][D];
+  float ml[NW][2];
+  HeadCtx ctx;
+};
+
+template <int D>
+__global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
+    k3_decode_mma(const __grid_constant__ DecParams p, const __grid_constant__ CUtensorMap tmK,
+                  const __grid_constant__ CUtensorMap tmV) {
+  using S = MmaShape<D>;
+  constexpr int NW = S::NW, RB = S::RB, PAGE = S::PAGE, KPW = S::KPW, TILES = S::TILES;
+  constexpr int NK = D / 16;  // 16-dim chunks
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
+  __shared__ __align__(8) uint64_t pub_full[2], pub_empty[2];
+  __shared__ PubSlot<NW, D> s_pub[2];
+  __shared__ int s_last;
+  __shared__ int hist[256];
+  __shared__ int red_i[33];
+  using ES = NamedSync<S::NE * 32, 2, S::EFIRST>;
+
+  const int G = p.G;
+  int* s_prefix = reinterpret_cast<int*>(smem + kStages * S::STAGE_B);
+  int* s_live = s_prefix + (G + 1);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  AKV_TRACE(0);
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], NW); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&pub_full[s], NW); mbar_init(&pub_empty[s], 1); }
+    mbar_fence_init();
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+  }
+  // PDL: everything above overlaps the previous step's tail; live_in and the
+  // arena are read only after the previous grid has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const long long P = plan_pages(p, PAGE, s_prefix, s_live, red_i);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  AKV_TRACE(1);
+  const int grid = (int)(P < (long long)gridDim.x ? P : (long long)gridDim.x);
+  if ((int)blockIdx.x >= grid) return;
+  const long long pbeg = (long long)blockIdx.x * P / grid;
+  const long long pend = (long long)(blockIdx.x + 1) * P / grid;
+  const int g0 = head_of_page(s_prefix, G, pbeg);
+
+  if (warp == NW) {  // ---------------- producer ----------------
+    if (lane == 0) {
+      const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
+      int g = g0, stage = 0;
+      uint32_t phase = 0;
+      for (long long pg = pbeg; pg < pend; ++pg) {
+        while (pg >= s_prefix[g + 1]) ++g;
+        const int L = s_live[g];
+        const int slot0 = (int)(pg - s_prefix[g]) * PAGE;
+        const int rows = max(0, min(PAGE, L - slot0));
+        const bool has_new = (L >= slot0 && L < slot0 + PAGE);
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* st = smem + stage * S::STAGE_B;
+        const int64_t base = p.seg_off[g];
+        const uint32_t meta_b = ((rows * 4) + 15) & ~15;
+        const uint32_t bytes = (rows ? 2u * kPageBytes + meta_b : 0u) + RB + (has_new ? 2 * RB : 0);
+        mbar_arrive_expect_tx(&full_bar[stage], bytes);
+        if (rows) {
+          const int row0 = (int)(base + slot0);
+#pragma unroll
+          for (int bx = 0; bx < S::NBOX; ++bx) {
+            tma_load_2d(st + bx * S::BOX_B, &tmK, bx * 64, row0, &full_bar[stage], pol_stream);
+            tma_load_2d(st + kPageBytes + bx * S::BOX_B, &tmV, bx * 64, row0, &full_bar[stage],
+                        pol_stream);
+          }
+          bulk_g2s(st + 2 * kPageBytes, p.meta + base + slot0, meta_b, &full_bar[stage], pol_keep);
+        }
+        uint8_t* hdr = st + S::HDR_OFF;
+        bulk_g2s(hdr, static_cast<const __nv_bfloat16*>(p.q) + (size_t)g * p.bh_stride, RB,
+                 &full_bar[stage], pol_keep);
+        if (has_new) {
+          bulk_g2s(hdr + RB, static_cast<const __nv_bfloat16*>(p.kn) + (size_t)g * p.bh_stride, RB,
+                   &full_bar[stage], pol_keep);
+          bulk_g2s(hdr + 2 * RB, static_cast<const __nv_bfloat16*>(p.vn) + (size_t)g * p.bh_stride,
+                   RB, &full_bar[stage], pol_keep);
+        }
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      }
+    }
+    return;
+  }
+
+  if (warp > NW) {  // ---------------- epilogue warps ----------------
+    // one published segment per head touched by this CTA's page range, in order
+    int pub_n = 0;
+    for (int g = g0; g < G && s_prefix[g] < pend; ++g) {
+      if (s_prefix[g + 1] == s_prefix[g]) continue;  // head without pages
+      const int slot = pub_n & 1;
+      mbar_wait(&pub_full[slot], (pub_n >> 1) & 1);
+      const HeadCtx hc = s_pub[slot].ctx;
+      publish_head<ES, NW, D>(p, hc, s_prefix, P, grid, s_pub[slot].red, s_pub[slot].ml, &s_last,
+                              RB / 16, hist, red_i, &pub_empty[slot]);
+      if (s_last && p.trace && ES::tid() == 0) {
+        atomicAdd(&p.trace[blockIdx.x * 8 + 5], 1ull);               // epilogues run
+        if (hc.freq) atomicAdd(&p.trace[blockIdx.x * 8 + 6], 1ull);  // frequent ones
+      }
+      ++pub_n;
+    }
+    if (p.trace && ES::tid() == 0) p.trace[blockIdx.x * 8 + 4] = gtimer();
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int gq = lane >> 2, qq = lane & 3;  // mma fragment coordinates
+  int pub_n = 0;
+  int g = g0, stage = 0;
+  uint32_t phase = 0;
+  HeadCtx hc;
+  hc.g = -1;
+  float m_run = -INFINITY, l_run = 0.f;
+  float o[NK][4];
+#pragma unroll
+  for (int t = 0; t < NK; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
+
+  for (long long pg = pbeg; pg < pend; ++pg) {
+    while (pg >= s_prefix[g + 1]) ++g;
+    if (g != hc.g) load_head(p, g, s_live[g], hc);
+    const int L = hc.L, n = hc.n;
+    const int slot0 = (int)(pg - s_prefix[g]) * PAGE;
+    mbar_wait(&full_bar[stage], phase);
+    if (pg == pbeg) AKV_TRACE(2);
+    uint8_t* st = smem + stage * S::STAGE_B;
+    const uint32_t kbase = smem_u32(st), vbase = smem_u32(st + kPageBytes);
+    const int* mpage = reinterpret_cast<const int*>(st + 2 * kPageBytes);
+    const uint8_t* hdr = st + S::HDR_OFF;
+    // the new token's row replaces its (stale) arena row in this warp's tile
+    const int wrow0 = warp * KPW;
+    if (L >= slot0 + wrow0 && L < slot0 + wrow0 + KPW) {
+      const int r = L - slot0;
+      const uint4* kn = reinterpret_cast<const uint4*>(hdr + RB);
+      const uint4* vn = reinterpret_cast<const uint4*>(hdr + 2 * RB);
+      for (int c = lane; c < 2 * (RB / 16); c += 32) {
+        const int cc = c % (RB / 16);
+        const uint4 val = c < RB / 16 ? kn[cc] : vn[cc];
+        *reinterpret_cast<uint4*>(st + (c < RB / 16 ? 0 : kPageBytes) + swz<D>(r, cc)) = val;
+        uint4* dstg = static_cast<uint4*>(c < RB / 16 ? p.kc : p.vc) + (hc.base + L) * (RB / 16);
+        st_v4(dstg + cc, val);  // fused insert into the arena
+      }
+      if (lane == 0) {
+        p.meta[hc.base + L] = p.pos | (hc.ncls << kClsShift);
+        p.score[hc.base + L] = 0.0;  // policies.py:357
+      }
+      fence_proxy_async_smem();  // generic writes precede the next TMA into this stage
+      __syncwarp();
+    }
+    // q as the B operand: column 0 of a 16x8 tile per 16-dim chunk
+    uint32_t qb[NK][2];
+#pragma unroll
+    for (int kk = 0; kk < NK; ++kk) {
+      if (gq == 0) {
+        qb[kk][0] = *reinterpret_cast<const uint32_t*>(hdr + (kk * 16 + 2 * qq) * 2);
+        qb[kk][1] = *reinterpret_cast<const uint32_t*>(hdr + (kk * 16 + 2 * qq + 8) * 2);
+      } else {
+        qb[kk][0] = qb[kk][1] = 0u;
+      }
+    }
+    // logits: lanes with qq == 0 own keys (gq) and (gq + 8) of each tile
+    float sx[TILES][2];
+    float pm = -INFINITY;
+#pragma unroll
+    for (int t = 0; t < TILES; ++t) {
+      const int r0 = wrow0 + t * 16;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      const int lr = r0 + ((lane >> 3) & 1) * 8 + (lane & 7);
+#pragma unroll
+      for (int kk = 0; kk < NK; ++kk) {
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4(kbase + swz<D>(lr, kk * 2 + (lane >> 4)), a0, a1, a2, a3);
+        mma_bf16(acc, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
+      }
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int row = r0 + gq + 8 * h2;
+        const int slot = slot0 + row;
+        float x = -INFINITY;
+        if (qq == 0 && slot < n) {
+          const int mt = slot < L ? mpage[row] : (p.pos | (hc.ncls << kClsShift));
+          x = biased_logit(acc[2 * h2] * p.scale, mt, hc, p.pos);
+          if (hc.freq && slot < L) p.logit[hc.base + slot] = x;
+        }
+        sx[t][h2] = x;
+        pm = fmaxf(pm, x);
+      }
+    }
+    pm = warp_allreduce(pm, [](float a, float b) { return fmaxf(a, b); });
+    const float m_new = fmaxf(m_run, pm);
+    if (m_new != -INFINITY) {
+      const float sc = (m_run == -INFINITY) ? 0.f : __expf(m_run - m_new);
+      l_run *= sc;
+#pragma unroll
+      for (int t = 0; t < NK; ++t) {
+        o[t][0] *= sc; o[t][1] *= sc; o[t][2] *= sc; o[t][3] *= sc;
+      }
+#pragma unroll
+      for (int t = 0; t < TILES; ++t) {
+        const int r0 = wrow0 + t * 16;
+        // p in bf16, packed (key gq | key gq+8) on the owning lanes
+        const __nv_bfloat16 p0 = __float2bfloat16_rn(sx[t][0] == -INFINITY ? 0.f : __expf(sx[t][0] - m_new));
+        const __nv_bfloat16 p1 = __float2bfloat16_rn(sx[t][1] == -INFINITY ? 0.f : __expf(sx[t][1] - m_new));
+        if (qq == 0) l_run += __bfloat162float(p0) + __bfloat162float(p1);
+        const uint32_t pk = (uint32_t)__bfloat16_as_ushort(p0) | ((uint32_t)__bfloat16_as_ushort(p1) << 16);
+        const uint32_t u = __shfl_sync(0xffffffffu, pk, 8 * qq);      // keys 2qq, 2qq+8
+        const uint32_t v = __shfl_sync(0xffffffffu, pk, 8 * qq + 4);  // keys 2qq+1, 2qq+9
+        const uint32_t b0 = gq == 0 ? __byte_perm(u, v, 0x5410) : 0u;
+        const uint32_t b1 = gq == 0 ? __byte_perm(u, v, 0x7632) : 0u;
+        const bool partial = slot0 + r0 + 16 > n;  // rows past the live tail hold stale data
+        const int lr = r0 + (lane >> 4) * 8 + (lane & 7);
+#pragma unroll
+        for (int tt = 0; tt < NK; ++tt) {
+          uint32_t a0, a1, a2, a3;
+          ldsm_x4_t(vbase + swz<D>(lr, tt * 2 + ((lane >> 3) & 1)), a0, a1, a2, a3);
+          if (partial) {  // zero V of keys >= n (0 * NaN would poison the sum)
+            const int k0 = slot0 + r0 + 2 * qq;
+            const uint32_t m0 = (k0 < n ? 0xffffu : 0u) | (k0 + 1 < n ? 0xffff0000u : 0u);
+            const uint32_t m8 = (k0 + 8 < n ? 0xffffu : 0u) | (k0 + 9 < n ? 0xffff0000u : 0u);
+            a0 &= m0; a1 &= m0; a2 &= m8; a3 &= m8;
+          }
+          mma_bf16(o[tt], a0, a1, a2, a3, b0, b1);
+        }
+      }
+      m_run = m_new;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[stage]);
+    if (++stage == kStages) { stage = 0; phase ^= 1; }
+
+    if (!((pg + 1 == pend) || (pg + 1 == s_prefix[g + 1]))) continue;
+    // hand the segment to the epilogue warps and keep streaming
+    l_run = warp_allreduce(l_run, [](float a, float b) { return a + b; });
+    {
+      const int slot = pub_n & 1;
+      mbar_wait(&pub_empty[slot], ((pub_n >> 1) & 1) ^ 1);
+      PubSlot<NW, D>& ps = s_pub[slot];
+      if (qq == 0) {
+#pragma unroll
+        for (int tt = 0; tt < NK; ++tt) {
+          ps.red[warp][tt * 16 + gq] = o[tt][0];
+          ps.red[warp][tt * 16 + gq + 8] = o[tt][2];
+        }
+      }
+      if (lane == 0) {
+        ps.ml[warp][0] = m_run;
+        ps.ml[warp][1] = l_run;
+        if (warp == 0) ps.ctx = hc;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pub_full[slot]);
+      ++pub_n;
+    }
+    if (pg + 1 == pend) AKV_TRACE(3);
+    m_run = -INFINITY;
+    l_run = 0.f;
+#pragma unroll
+    for (int t = 0; t < NK; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
+  }
+}
+
+// ===========================================================================
+static int g_num_sms = 0;
+unsigned long long* g_dec_trace = nullptr;  // set by akv_debug_set_decode_trace
+
+static cudaError_t num_sms(int* out) {
+  if (!g_num_sms) {
+    int dev;
+    cudaError_t e;
+    if ((e = cudaGetDevice(&dev))) return e;
+    if ((e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev))) return e;
+  }
+  *out = g_num_sms;
+  return cudaSuccess;
+}
+
+// Launch with programmatic dependent launch: the next step's CTAs start
+// their prologue while this step drains (griddepcontrol in the kernels).
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 template <typename T, int D>
-static cudaError_t launch_decode(const DecParams& p, int G, cudaStream_t st) {
-  dim3 grid(p.max_chunks, G);
-  k3_decode<T, D><<<grid, kDecWarps * 32, 0, st>>>(p);
-  return cudaGetLastError();
+static cudaError_t launch_simt(const DecParams& p, cudaStream_t st) {
+  using S = SimtShape<T, D>;
+  auto kern = k3_decode_simt<T, D>;
+  static bool attr = false;
+  cudaError_t e;
+  if (!attr) {
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(kStages * S::STAGE_B + (2 * kMaxHeads + 1) * 4))))
+      return e;
+    attr = true;
+  }
+  int sms;
+  if ((e = num_sms(&sms))) return e;
+  const size_t smem = (size_t)kStages * S::STAGE_B + (size_t)(2 * p.G + 1) * 4;
+  return launch_pdl(kern, 2 * sms, S::NW * 32 + 32, smem, st, p);
+}
+
+// tensor maps of the arena, cached per (base, slots) so steady-state steps
+// (and CUDA-graph capture) do no host-side encoding
+struct TmapCache {
+  const void* kc = nullptr;
+  const void* vc = nullptr;
+  int64_t slots = -1;
+  int d = 0;
+  CUtensorMap k, v;
+};
+static thread_local TmapCache g_tmaps;
+
+template <int D>
+static cudaError_t launch_mma(const DecParams& p, int64_t total_slots, cudaStream_t st) {
+  using S = MmaShape<D>;
+  if (g_tmaps.kc != p.kc || g_tmaps.vc != p.vc || g_tmaps.slots != total_slots || g_tmaps.d != D) {
+    if (!encode_tmap_2d_bf16(&g_tmaps.k, p.kc, (uint64_t)total_slots, D, 64, S::PAGE, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !encode_tmap_2d_bf16(&g_tmaps.v, p.vc, (uint64_t)total_slots, D, 64, S::PAGE, CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+    g_tmaps.kc = p.kc; g_tmaps.vc = p.vc; g_tmaps.slots = total_slots; g_tmaps.d = D;
+  }
+  auto kern = k3_decode_mma<D>;
+  static bool attr = false;
+  cudaError_t e;
+  if (!attr) {
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(1024 + kStages * S::STAGE_B + (2 * kMaxHeads + 1) * 4))))
+      return e;
+    attr = true;
+  }
+  int sms;
+  if ((e = num_sms(&sms))) return e;
+  const size_t smem = 1024 + (size_t)kStages * S::STAGE_B + (size_t)(2 * p.G + 1) * 4;
+  return launch_pdl(kern, 2 * sms, S::THREADS, smem, st, p, g_tmaps.k, g_tmaps.v);
 }
 
 struct DecWs {
@@ -349,19 +1259,26 @@ struct DecWs {
   int32_t* counter;
   int32_t* status;
   size_t bytes;
-  int max_chunks;
+  int max_parts;
 };
+
+// partial slots per head: one per contributing CTA, bounded by the head's
+// page count (smallest page over dtypes for this head dim: fp32 rows)
+static inline int max_parts_for(int d, int max_cap) {
+  const int page = kPageBytes / (d * 4);
+  return (max_cap + page - 1) / page + 1;
+}
 
 static DecWs carve(void* ws, int B, int H, int d, int max_cap, int64_t total_slots) {
   DecWs w;
   const int G = B * H;
-  w.max_chunks = (max_cap + min_chunk(d) - 1) / min_chunk(d);
+  w.max_parts = max_parts_for(d, max_cap);
   char* c = static_cast<char*>(ws);
   size_t off = 0;
   auto take = [&](size_t bytes) { char* r = c + off; off += (bytes + 255) & ~size_t(255); return r; };
   w.counter = reinterpret_cast<int32_t*>(take((size_t)G * 4));
   w.status = reinterpret_cast<int32_t*>(take(4));
-  w.part = reinterpret_cast<float*>(take((size_t)G * w.max_chunks * (d + 2) * 4));
+  w.part = reinterpret_cast<float*>(take((size_t)G * w.max_parts * (d + 2) * 4));
   w.logit = reinterpret_cast<float*>(take((size_t)total_slots * 4));
   w.bytes = off;
   return w;
@@ -370,6 +1287,12 @@ static DecWs carve(void* ws, int B, int H, int d, int max_cap, int64_t total_slo
 }  // namespace akv
 
 using namespace akv;
+
+// Debug hook (not part of the ABI header): record per-CTA timestamps of
+// the next decode launches into a device buffer of [2*SMs, 8] uint64.
+extern "C" void akv_debug_set_decode_trace(void* buf) {
+  g_dec_trace = static_cast<unsigned long long*>(buf);
+}
 
 extern "C" size_t akv_decode_workspace_size(int32_t B, int32_t H, int32_t d, int32_t max_cap,
                                            int64_t total_slots) {
@@ -380,7 +1303,6 @@ extern "C" int akv_decode_workspace_init(void* ws, size_t bytes, int32_t B, int3
                                          int32_t max_cap, int64_t total_slots, void* stream) {
   DecWs w = carve(ws, B, H, d, max_cap, total_slots);
   if (bytes < w.bytes) return set_error(AKV_ERR_CAPACITY, "akv_decode_workspace_init: workspace too small");
-  // counters + status are contiguous at the start
   cudaError_t e = cudaMemsetAsync(ws, 0, reinterpret_cast<char*>(w.part) - static_cast<char*>(ws),
                                   static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return set_error(AKV_ERR_CUDA, "akv_decode_workspace_init: %s", cudaGetErrorString(e));
@@ -390,6 +1312,8 @@ extern "C" int akv_decode_workspace_init(void* ws, size_t bytes, int32_t B, int3
 extern "C" int akv_decode_step(const akv_decode_args* a, void* stream) {
   if (!a) return set_error(AKV_ERR_INVALID, "akv_decode_step: null args");
   if (a->B < 1 || a->H < 1) return set_error(AKV_ERR_INVALID, "akv_decode_step: empty input");
+  if (a->B * a->H > kMaxHeads)
+    return set_error(AKV_ERR_UNSUPPORTED, "akv_decode_step: more than %d heads per launch", kMaxHeads);
   if (a->pos < a->prompt_len || a->prompt_len < 1)
     return set_error(AKV_ERR_INVALID, "akv_decode_step: need pos >= prompt_len >= 1");
   if (a->pos > kPosMask) return set_error(AKV_ERR_UNSUPPORTED, "akv_decode_step: position too large");
@@ -398,39 +1322,34 @@ extern "C" int akv_decode_step(const akv_decode_args* a, void* stream) {
   if (a->bh_stride < a->d) return set_error(AKV_ERR_INVALID, "akv_decode_step: bh_stride < d");
   DecWs w = carve(a->workspace_dev, a->B, a->H, a->d, a->max_cap, a->total_slots);
   if (a->workspace_bytes < w.bytes) return set_error(AKV_ERR_CAPACITY, "akv_decode_step: workspace too small");
-  DecParams p{a->B, a->H, a->prompt_len, a->pos, a->q_dev, a->k_dev, a->v_dev, a->bh_stride,
-              a->new_cls_dev, a->slope_dev, a->sink_dev, a->head_atoms_dev, a->head_r_l_dev,
-              a->head_r_f_dev, a->seg_off_dev, a->seg_cap_dev, a->kc_dev, a->vc_dev, a->meta_dev,
-              a->score_dev, a->live_in_dev, a->live_out_dev, a->out_dev, a->evicted_dev,
-              a->status_dev ? a->status_dev : w.status, w.part, w.logit, w.counter, 0,
-              (float)(1.0 / sqrt((double)a->d))};
-  const int G = a->B * a->H;
+  DecParams p{a->B, a->H, a->B * a->H, a->prompt_len, a->pos, a->q_dev, a->k_dev, a->v_dev,
+              a->bh_stride, a->new_cls_dev, a->slope_dev, a->sink_dev, a->head_atoms_dev,
+              a->head_r_l_dev, a->head_r_f_dev, a->seg_off_dev, a->seg_cap_dev, a->kc_dev, a->vc_dev,
+              a->meta_dev, a->score_dev, a->live_in_dev, a->live_out_dev, a->out_dev,
+              a->evicted_dev, a->status_dev ? a->status_dev : w.status, w.part, w.logit, w.counter,
+              w.max_parts, (float)(1.0 / sqrt((double)a->d)), g_dec_trace};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaErrorInvalidValue;
   bool ok = true;
-#define AKV_DEC(T, DD)                                              \
-  p.max_chunks = (a->max_cap + DecShape<T, DD>::C - 1) / DecShape<T, DD>::C; \
-  e = launch_decode<T, DD>(p, G, st);
   if (a->dtype == AKV_DTYPE_BF16) {
     switch (a->d) {
-      case 16: AKV_DEC(__nv_bfloat16, 16) break;
-      case 32: AKV_DEC(__nv_bfloat16, 32) break;
-      case 64: AKV_DEC(__nv_bfloat16, 64) break;
-      case 128: AKV_DEC(__nv_bfloat16, 128) break;
+      case 16: e = launch_simt<__nv_bfloat16, 16>(p, st); break;
+      case 32: e = launch_simt<__nv_bfloat16, 32>(p, st); break;
+      case 64: e = g_disable_tc ? launch_simt<__nv_bfloat16, 64>(p, st) : launch_mma<64>(p, a->total_slots, st); break;
+      case 128: e = g_disable_tc ? launch_simt<__nv_bfloat16, 128>(p, st) : launch_mma<128>(p, a->total_slots, st); break;
       default: ok = false;
     }
   } else if (a->dtype == AKV_DTYPE_F32) {
     switch (a->d) {
-      case 16: AKV_DEC(float, 16) break;
-      case 32: AKV_DEC(float, 32) break;
-      case 64: AKV_DEC(float, 64) break;
-      case 128: AKV_DEC(float, 128) break;
+      case 16: e = launch_simt<float, 16>(p, st); break;
+      case 32: e = launch_simt<float, 32>(p, st); break;
+      case 64: e = launch_simt<float, 64>(p, st); break;
+      case 128: e = launch_simt<float, 128>(p, st); break;
       default: ok = false;
     }
   } else {
     ok = false;
   }
-#undef AKV_DEC
   if (!ok) return set_error(AKV_ERR_UNSUPPORTED, "akv_decode_step: unsupported dtype %d / head dim %d", a->dtype, a->d);
   if (e != cudaSuccess) return set_error(AKV_ERR_CUDA, "akv_decode_step: %s", cudaGetErrorString(e));
   return AKV_OK;
