@@ -71,3 +71,7 @@ bool encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint
   return r == CUDA_SUCCESS;
 }
 }  // namespace akv
+
+// Debug hook (not part of the ABI header): enable/disable the tensor-core
+// paths at run time (tests cross-check them against the SIMT passes).
+extern "C" void akv_debug_set_tc(int enable) { akv::g_disable_tc = !enable; }

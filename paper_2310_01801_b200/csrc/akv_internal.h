@@ -11,6 +11,7 @@ namespace akv {
 
 // tcgen05/TMA profiling passes for bf16, head dim 128 (akv_profile_tc.cu).
 bool tc_profile_supported(int N);
+int tc_tiles(int N);  // 128-key tiles of the tensor-core passes (out_part rows per head)
 cudaError_t launch_tc_passes(const void* q, const void* k, const void* v, int B, int H, int N,
                              int64_t ld, const uint8_t* cls, int64_t cls_ld, const float* slope,
                              const float* sink, float* lse, double* colsum, double* colsq,

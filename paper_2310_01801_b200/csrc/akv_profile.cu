@@ -457,7 +457,9 @@ extern "C" int akv_profile(const akv_profile_args* a, void* stream) {
                 static_cast<float*>(a->workspace_dev)};
   cudaError_t e = cudaErrorInvalidValue;
   bool done = false;
+  int part_tiles = ntiles;  // out_part rows per head (64-key SIMT tiles / 128-key TC tiles)
   if (a->dtype == AKV_DTYPE_BF16 && a->d == 128 && tc_profile_supported(a->N)) {
+    part_tiles = tc_tiles(a->N);
     e = launch_tc_passes(pp.q, pp.k, pp.v, a->B, a->H, a->N, a->ld, a->cls_dev, a->cls_ld,
                          a->slope_dev, a->sink_dev, a->lse_dev, a->colsum_dev, a->colsq_dev,
                          a->lastp_dev, pp.out_part, st);
@@ -488,7 +490,7 @@ extern "C" int akv_profile(const akv_profile_args* a, void* stream) {
   if (e != cudaSuccess) return set_error(AKV_ERR_CUDA, "akv_profile: %s", cudaGetErrorString(e));
 
   PolicyParams pol{};
-  pol.B = a->B; pol.H = a->H; pol.N = a->N; pol.d = a->d; pol.ntiles = ntiles;
+  pol.B = a->B; pol.H = a->H; pol.N = a->N; pol.d = a->d; pol.ntiles = part_tiles;
   pol.cls = a->cls_dev; pol.cls_ld = a->cls_ld;
   pol.colsum = a->colsum_dev; pol.colsq = a->colsq_dev; pol.lastp = a->lastp_dev;
   pol.out_part = pp.out_part;

@@ -1,12 +1,363 @@
-// tcgen05/TMA profiling passes (bf16, head dim 128) — placeholder until the
-// tensor-core passes land; the SIMT passes in akv_profile.cu serve all shapes.
+// K1 on the 5th-generation tensor cores: tcgen05.mma + TMA + TMEM passes of
+// the prompt profiler for bf16 Q/K/V with head dim 128 (akv_profile routes
+// here; the SIMT passes in akv_profile.cu serve fp32 and other head dims).
+//
+// Pass 1 (query-major) — per (head, 128-query tile): S = Q_i K_j^T for key
+//   tiles j <= i, 128x128x128 per tcgen05.mma group into a double-buffered
+//   TMEM accumulator; the epilogue warps (one TMEM lane = one query row)
+//   fold each tile into the row's online (max, sum) in the exp2 domain and
+//   finally write lse_i (attention.py:64-89 normaliser).
+// Pass 2 (key-major, recomputed) — per (head, 128-key tile): S^T = K_j Q_i^T
+//   for query tiles i >= j, so a TMEM lane is a key and the column sums are
+//   per-thread register reductions (no shuffles, no atomics):
+//   colsum_j = sum_i exp(s_ij - lse_i) (engine.py:196), its square sum
+//   (profiler.py:148-161 cosine), the prompt's last row A[N-1, :] and the
+//   last-row output partial A[N-1, tile] @ V[tile] (engine.py:248,255).
+// Warp roles per CTA (192 threads): warp 0 TMA producer, warp 1 TMEM owner
+// and single-thread MMA issuer, warps 2-5 epilogue.  The fixed operand (Q
+// tile in pass 1, K tile in pass 2) is loaded once; the streamed operand
+// goes through a 2-stage ring.  Grid blocks are ordered heaviest first.
+
+#include <math.h>
+
+#include "akv_common.cuh"
 #include "akv_internal.h"
+#include "akv_tc.cuh"
 
 namespace akv {
-bool tc_profile_supported(int N) { (void)N; return false; }
-cudaError_t launch_tc_passes(const void*, const void*, const void*, int, int, int, int64_t,
-                             const uint8_t*, int64_t, const float*, const float*, float*, double*,
-                             double*, float*, float*, cudaStream_t) {
-  return cudaErrorNotSupported;
+
+constexpr int kTT = 128;                   // tile edge (queries / keys)
+constexpr int kBoxB = 128 * 128;           // one 128-row x 64-col bf16 box (16 KB)
+constexpr int kTileB = 2 * kBoxB;          // 128 x 128 bf16 tile (32 KB)
+constexpr int kRing = 2;                   // streamed-operand stages
+constexpr int kTcThreads = 192;            // warp0 TMA, warp1 MMA/TMEM, warps 2-5 epilogue
+constexpr uint32_t kTmemCols = 256;        // two 128-column fp32 accumulators
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr size_t kTcSmem = 1024 + (size_t)(1 + kRing) * kTileB;
+
+struct TcParams {
+  int H, N;
+  int64_t ld;
+  const uint8_t* cls;
+  int64_t cls_ld;
+  const float* slope;
+  const float* sink;
+  const __nv_bfloat16* v;
+  float* lse;
+  double* colsum;
+  double* colsq;
+  float* lastp;
+  float* out_part;  // [G, ntiles, 128]
+  float scale;
+};
+
+using EpiSync = NamedSync<128, 1, 64>;
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
+
+// issue the 8 K=16 steps of one 128x128x128 tile product
+__device__ __forceinline__ void mma_tile(uint32_t tmem_d, const uint8_t* a_tile,
+                                         const uint8_t* b_tile) {
+  constexpr uint32_t idesc = umma_idesc_bf16(128, 128);
+  const uint32_t a0 = smem_u32(a_tile), b0 = smem_u32(b_tile);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t off = (k >> 2) * kBoxB + (k & 3) * 32;
+    umma_bf16_ss(tmem_d, umma_desc_sw128(a0 + off), umma_desc_sw128(b0 + off), idesc, k > 0);
+  }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kTcThreads, 2)
+    k1tc_rowlse(const __grid_constant__ TcParams p, const __grid_constant__ CUtensorMap tmQ,
+                const __grid_constant__ CUtensorMap tmK) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sQ = smem;
+  uint8_t* sK = smem + kTileB;
+  __shared__ __align__(8) uint64_t q_full, k_full[kRing], k_empty[kRing], acc_full[2], acc_empty[2];
+  __shared__ uint32_t s_tmem;
+  __shared__ float s_col[2][kTT];
+  const int ntiles = (p.N + kTT - 1) / kTT;
+  const int g = blockIdx.y, h = g % p.H, b = g / p.H;
+  const int qt = ntiles - 1 - blockIdx.x;  // heaviest (most key tiles) first
+  const int nk = qt + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(&q_full, 1);
+    for (int s = 0; s < kRing; ++s) { mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&acc_full[a], 1); mbar_init(&acc_empty[a], 4); }
+    mbar_fence_init();
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+  }
+  if (warp == 1) tmem_alloc(&s_tmem, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+
+  if (warp == 0) {  // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      const uint64_t pol_q = policy_evict_first(), pol_k = policy_evict_last();
+      const int rq = (int)((int64_t)g * p.ld + (int64_t)qt * kTT);
+      mbar_arrive_expect_tx(&q_full, kTileB);
+      tma_load_2d(sQ, &tmQ, 0, rq, &q_full, pol_q);
+      tma_load_2d(sQ + kBoxB, &tmQ, 64, rq, &q_full, pol_q);
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % kRing;
+        mbar_wait(&k_empty[s], ((kt / kRing) & 1) ^ 1);
+        mbar_arrive_expect_tx(&k_full[s], kTileB);
+        const int rk = (int)((int64_t)g * p.ld + (int64_t)kt * kTT);
+        tma_load_2d(sK + s * kTileB, &tmK, 0, rk, &k_full[s], pol_k);
+        tma_load_2d(sK + s * kTileB + kBoxB, &tmK, 64, rk, &k_full[s], pol_k);
+      }
+    }
+  } else if (warp == 1) {  // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      mbar_wait(&q_full, 0);
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % kRing, a = kt & 1;
+        mbar_wait(&k_full[s], (kt / kRing) & 1);
+        mbar_wait(&acc_empty[a], ((kt >> 1) & 1) ^ 1);
+        tc_fence_after();
+        mma_tile(tmem + a * kTT, sQ, sK + s * kTileB);
+        umma_commit(&k_empty[s]);
+        umma_commit(&acc_full[a]);
+      }
+    }
+  } else {  // ---------------- epilogue (warps 2-5) ----------------
+    const int quarter = warp & 3;
+    const int et = threadIdx.x - 64;
+    const int row = qt * kTT + quarter * 32 + lane;
+    const float sl2 = p.scale * kLog2e;
+    const float slope_l2 = (p.slope ? p.slope[h] : 0.f) * kLog2e;
+    const float sink_l2 = (p.sink ? p.sink[h] : 0.f) * kLog2e;
+    const bool bias = slope_l2 != 0.f || sink_l2 != 0.f;
+    const uint8_t* cls = p.cls + (size_t)b * p.cls_ld;
+    const float rowterm = -slope_l2 * (float)row;
+    float m = -INFINITY, l = 0.f;
+    uint8_t cnext = 0;
+    if (bias) cnext = et < p.N ? cls[et] : 0;
+    for (int kt = 0; kt < nk; ++kt) {
+      const int a = kt & 1;
+      if (bias) {  // per-column bias of this key tile: sink on special keys + slope * col
+        const int col = kt * kTT + et;
+        s_col[a][et] = (cnext == AKV_CLS_SPECIAL ? sink_l2 : 0.f) + slope_l2 * (float)col;
+        const int nc = col + kTT;
+        cnext = (kt + 1 < nk && nc < p.N) ? cls[nc] : 0;
+        EpiSync::sync();
+      }
+      mbar_wait(&acc_full[a], (kt >> 1) & 1);
+      tc_fence_after();
+      const bool diag = (kt == qt);
+      const bool tail = (kt + 1) * kTT > p.N;
+#pragma unroll 1
+      for (int ch = 0; ch < 4; ++ch) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + a * kTT + ch * 32, v);
+        float cm = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const int col = kt * kTT + ch * 32 + c;
+          float x = v[c] * sl2;
+          if (bias) x += s_col[a][ch * 32 + c] + rowterm;
+          if ((diag && col > row) || (tail && col >= p.N)) x = -INFINITY;
+          v[c] = x;
+          cm = fmaxf(cm, x);
+        }
+        const float mn = fmaxf(m, cm);
+        if (mn != -INFINITY) {
+          float sum = 0.f;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) sum += fast_exp2(v[c] - mn);
+          l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + sum;
+          m = mn;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[a]);
+    }
+    if (row < p.N) p.lse[(size_t)g * p.N + row] = (m + __log2f(l)) * kLn2;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kTcThreads, 2)
+    k1tc_colsum(const __grid_constant__ TcParams p, const __grid_constant__ CUtensorMap tmQ,
+                const __grid_constant__ CUtensorMap tmK) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sK = smem;
+  uint8_t* sQ = smem + kTileB;
+  __shared__ __align__(8) uint64_t k_full, q_full[kRing], q_empty[kRing], acc_full[2], acc_empty[2];
+  __shared__ uint32_t s_tmem;
+  __shared__ float s_col[2][kTT];
+  __shared__ float s_lastp[kTT];
+  const int ntiles = (p.N + kTT - 1) / kTT;
+  const int g = blockIdx.y, h = g % p.H, b = g / p.H;
+  const int kt = blockIdx.x;  // key tile 0 sees the most query tiles: first
+  const int nq = ntiles - kt;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(&k_full, 1);
+    for (int s = 0; s < kRing; ++s) { mbar_init(&q_full[s], 1); mbar_init(&q_empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&acc_full[a], 1); mbar_init(&acc_empty[a], 4); }
+    mbar_fence_init();
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+  }
+  if (warp == 1) tmem_alloc(&s_tmem, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+
+  if (warp == 0) {  // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      const uint64_t pol_k = policy_evict_first(), pol_q = policy_evict_last();
+      const int rk = (int)((int64_t)g * p.ld + (int64_t)kt * kTT);
+      mbar_arrive_expect_tx(&k_full, kTileB);
+      tma_load_2d(sK, &tmK, 0, rk, &k_full, pol_k);
+      tma_load_2d(sK + kBoxB, &tmK, 64, rk, &k_full, pol_k);
+      for (int i = 0; i < nq; ++i) {
+        const int s = i % kRing;
+        mbar_wait(&q_empty[s], ((i / kRing) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[s], kTileB);
+        const int rq = (int)((int64_t)g * p.ld + (int64_t)(kt + i) * kTT);
+        tma_load_2d(sQ + s * kTileB, &tmQ, 0, rq, &q_full[s], pol_q);
+        tma_load_2d(sQ + s * kTileB + kBoxB, &tmQ, 64, rq, &q_full[s], pol_q);
+      }
+    }
+  } else if (warp == 1) {  // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      mbar_wait(&k_full, 0);
+      for (int i = 0; i < nq; ++i) {
+        const int s = i % kRing, a = i & 1;
+        mbar_wait(&q_full[s], (i / kRing) & 1);
+        mbar_wait(&acc_empty[a], ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+        mma_tile(tmem + a * kTT, sK, sQ + s * kTileB);  // S^T: keys on TMEM lanes
+        umma_commit(&q_empty[s]);
+        umma_commit(&acc_full[a]);
+      }
+    }
+  } else {  // ---------------- epilogue (warps 2-5) ----------------
+    const int quarter = warp & 3;
+    const int et = threadIdx.x - 64;
+    const int key = kt * kTT + quarter * 32 + lane;
+    const float sl2 = p.scale * kLog2e;
+    const float slope_l2 = (p.slope ? p.slope[h] : 0.f) * kLog2e;
+    const float sink_l2 = (p.sink ? p.sink[h] : 0.f) * kLog2e;
+    const uint8_t* cls = p.cls + (size_t)b * p.cls_ld;
+    const float* lse = p.lse + (size_t)g * p.N;
+    // per-key term: sink on a special key, + slope * key
+    const float kterm = (key < p.N && cls[key] == AKV_CLS_SPECIAL ? sink_l2 : 0.f) +
+                        slope_l2 * (float)key;
+    double dsum = 0.0, dsq = 0.0;
+    float lastp = 0.f;
+    const int qlast = p.N - 1;
+    int q0 = kt * kTT + et;
+    float lnext = q0 < p.N ? lse[q0] : 0.f;
+    for (int i = 0; i < nq; ++i) {
+      const int a = i & 1;
+      const int qt = kt + i;
+      {  // per-query term of this tile: -lse_q * log2e - slope * q
+        const int q = qt * kTT + et;
+        s_col[a][et] = -lnext * kLog2e - slope_l2 * (float)q;
+        const int qn = q + kTT;
+        lnext = (i + 1 < nq && qn < p.N) ? lse[qn] : 0.f;
+        EpiSync::sync();
+      }
+      mbar_wait(&acc_full[a], (i >> 1) & 1);
+      tc_fence_after();
+      const bool diag = (i == 0);
+      const bool tail = (qt + 1) * kTT > p.N;
+      float tsum = 0.f, tsq = 0.f;
+#pragma unroll 1
+      for (int ch = 0; ch < 4; ++ch) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + a * kTT + ch * 32, v);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const int q = qt * kTT + ch * 32 + c;
+          float pr = fast_exp2(fmaf(v[c], sl2, kterm + s_col[a][ch * 32 + c]));
+          if ((diag && q < key) || (tail && q >= p.N)) pr = 0.f;
+          tsum += pr;
+          tsq = fmaf(pr, pr, tsq);
+          if (q == qlast) lastp = pr;
+        }
+      }
+      dsum += (double)tsum;
+      dsq += (double)tsq;
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[a]);
+    }
+    if (key >= p.N) lastp = 0.f;
+    if (key < p.N) {
+      p.colsum[(size_t)g * p.N + key] = dsum;
+      p.colsq[(size_t)g * p.N + key] = dsq;
+      p.lastp[(size_t)g * p.N + key] = lastp;
+    }
+    s_lastp[quarter * 32 + lane] = lastp;
+    EpiSync::sync();
+    // last-row output partial of this key tile: sum_j lastp_j V_j (d = 128 = one dim per thread)
+    const __nv_bfloat16* vt = p.v + ((size_t)g * p.ld + (size_t)kt * kTT) * 128;
+    const int nrow = min(kTT, p.N - kt * kTT);
+    float o = 0.f;
+    for (int j = 0; j < nrow; ++j) o = fmaf(s_lastp[j], __bfloat162float(vt[(size_t)j * 128 + et]), o);
+    p.out_part[((size_t)g * ntiles + kt) * 128 + et] = o;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
+bool tc_profile_supported(int N) { return !g_disable_tc && N >= 1; }
+
+int tc_tiles(int N) { return (N + kTT - 1) / kTT; }
+
+cudaError_t launch_tc_passes(const void* q, const void* k, const void* v, int B, int H, int N,
+                             int64_t ld, const uint8_t* cls, int64_t cls_ld, const float* slope,
+                             const float* sink, float* lse, double* colsum, double* colsq,
+                             float* lastp, float* out_part, cudaStream_t st) {
+  const int G = B * H;
+  const uint64_t rows = (uint64_t)G * (uint64_t)ld;
+  if (rows >= (1ull << 31)) return cudaErrorInvalidValue;
+  CUtensorMap tmQ, tmK;
+  if (!encode_tmap_2d_bf16(&tmQ, q, rows, 128, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !encode_tmap_2d_bf16(&tmK, k, rows, 128, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  static bool attr = false;
+  cudaError_t e;
+  if (!attr) {
+    if ((e = cudaFuncSetAttribute(k1tc_rowlse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem)))
+      return e;
+    if ((e = cudaFuncSetAttribute(k1tc_colsum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem)))
+      return e;
+    attr = true;
+  }
+  TcParams p{H, N, ld, cls, cls_ld, slope, sink, static_cast<const __nv_bfloat16*>(v), lse, colsum,
+             colsq, lastp, out_part, (float)(1.0 / sqrt(128.0))};
+  const dim3 grid(tc_tiles(N), G);
+  k1tc_rowlse<<<grid, kTcThreads, kTcSmem, st>>>(p, tmQ, tmK);
+  if ((e = cudaGetLastError())) return e;
+  k1tc_colsum<<<grid, kTcThreads, kTcSmem, st>>>(p, tmQ, tmK);
+  return cudaGetLastError();
+}
+
 }  // namespace akv
