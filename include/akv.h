@@ -124,7 +124,15 @@ typedef struct akv_compact_args {
   const int32_t* kept_pos_dev;   /* [B*H,N] from akv_profile */
   const int32_t* kept_count_dev; /* [B*H] */
   const double* colsum_dev;      /* [B*H,N] scores copied for FREQUENT heads */
-  const uint8_t* head_atoms_dev; /* [B*H] atoms of each head's chosen policy */
+  const int8_t* choice_dev;      /* [B*H,choice_stride] from akv_profile; column 0 is used */
+  int32_t choice_stride;
+  int32_t n_family;              /* the family akv_profile chose from */
+  uint8_t family_atoms[AKV_MAX_FAMILY];
+  double family_r_l[AKV_MAX_FAMILY];
+  double family_r_f[AKV_MAX_FAMILY];
+  uint8_t* head_atoms_dev;       /* [B*H] out: atoms of each head's chosen policy */
+  double* head_r_l_dev;          /* [B*H] out: its r_l */
+  double* head_r_f_dev;          /* [B*H] out: its r_f */
   const int64_t* seg_off_dev;    /* [B*H] first slot of each head's segment */
   const int32_t* seg_cap_dev;    /* [B*H] segment capacity (slots) */
   void* kc_dev;                  /* [total_slots,d] compressed K (dtype) */

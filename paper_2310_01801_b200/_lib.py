@@ -46,7 +46,10 @@ class CompactArgs(C.Structure):
     _fields_ = [
         ("B", i32), ("H", i32), ("N", i32), ("d", i32), ("dtype", i32),
         ("k_dev", P), ("v_dev", P), ("ld", i64), ("cls_dev", P), ("cls_ld", i64),
-        ("kept_pos_dev", P), ("kept_count_dev", P), ("colsum_dev", P), ("head_atoms_dev", P),
+        ("kept_pos_dev", P), ("kept_count_dev", P), ("colsum_dev", P), ("choice_dev", P),
+        ("choice_stride", i32), ("n_family", i32), ("family_atoms", C.c_uint8 * MAX_FAMILY),
+        ("family_r_l", f64 * MAX_FAMILY), ("family_r_f", f64 * MAX_FAMILY),
+        ("head_atoms_dev", P), ("head_r_l_dev", P), ("head_r_f_dev", P),
         ("seg_off_dev", P), ("seg_cap_dev", P), ("kc_dev", P), ("vc_dev", P),
         ("meta_dev", P), ("score_dev", P), ("live_dev", P),
     ]

@@ -25,7 +25,15 @@ struct CompactParams {
   const int32_t* kept_pos;
   const int32_t* kept_count;
   const double* colsum;
-  const uint8_t* atoms;
+  const int8_t* choice;
+  int choice_stride;
+  int n_family;
+  uint8_t fam_atoms[AKV_MAX_FAMILY];
+  double fam_r_l[AKV_MAX_FAMILY];
+  double fam_r_f[AKV_MAX_FAMILY];
+  uint8_t* atoms;
+  double* r_l;
+  double* r_f;
   const int64_t* seg_off;
   const int32_t* seg_cap;
   uint4* kc;
@@ -40,8 +48,16 @@ __global__ void __launch_bounds__(128) k2_compact(CompactParams p) {
   const int kept = p.kept_count[g];
   const int cap = p.seg_cap[g];
   const int i0 = blockIdx.x * kCompactRows;
-  // a segment too small for its kept rows is reported as live = -1
-  if (blockIdx.x == 0 && threadIdx.x == 0) p.live[g] = kept > cap ? -1 : kept;
+  int c = p.choice[(size_t)g * p.choice_stride];
+  c = (c >= 0 && c < p.n_family) ? c : p.n_family - 1;
+  const uint8_t at = p.fam_atoms[c];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // a segment too small for its kept rows is reported as live = -1
+    p.live[g] = kept > cap ? -1 : kept;
+    p.atoms[g] = at;  // per-head policy table for decode
+    p.r_l[g] = p.fam_r_l[c];
+    p.r_f[g] = p.fam_r_f[c];
+  }
   if (i0 >= kept || kept > cap) return;
   const int nrows = min(kCompactRows, kept - i0);
   const int64_t base = p.seg_off[g];
@@ -58,7 +74,7 @@ __global__ void __launch_bounds__(128) k2_compact(CompactParams p) {
     st_v4(p.kc + dst, kv);
     st_v4(p.vc + dst, vv);
   }
-  const bool freq = (p.atoms[g] & AKV_ATOM_FREQUENT) && !(p.atoms[g] & AKV_ATOM_FULL);
+  const bool freq = (at & AKV_ATOM_FREQUENT) && !(at & AKV_ATOM_FULL);
   for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
     const int pos = kp[i0 + r];
     const int64_t slot = base + i0 + r;
@@ -101,12 +117,21 @@ extern "C" int akv_compact(const akv_compact_args* a, void* stream) {
   const int es = a->dtype == AKV_DTYPE_BF16 ? 2 : a->dtype == AKV_DTYPE_F32 ? 4 : 0;
   if (!es || (a->d * es) % 16 || a->d * es > 512)
     return set_error(AKV_ERR_UNSUPPORTED, "akv_compact: unsupported dtype %d / head dim %d", a->dtype, a->d);
-  CompactParams p{a->H, a->N, a->d * es / 16,
-                  static_cast<const uint4*>(a->k_dev), static_cast<const uint4*>(a->v_dev), a->ld,
-                  a->cls_dev, a->cls_ld, a->kept_pos_dev, a->kept_count_dev, a->colsum_dev,
-                  a->head_atoms_dev, a->seg_off_dev, a->seg_cap_dev,
-                  static_cast<uint4*>(a->kc_dev), static_cast<uint4*>(a->vc_dev), a->meta_dev,
-                  a->score_dev, a->live_dev};
+  if (a->n_family < 1 || a->n_family > AKV_MAX_FAMILY || a->choice_stride < 1)
+    return set_error(AKV_ERR_INVALID, "akv_compact: bad family / choice stride");
+  CompactParams p{};
+  p.H = a->H; p.N = a->N; p.row_vecs = a->d * es / 16;
+  p.k = static_cast<const uint4*>(a->k_dev); p.v = static_cast<const uint4*>(a->v_dev); p.ld = a->ld;
+  p.cls = a->cls_dev; p.cls_ld = a->cls_ld;
+  p.kept_pos = a->kept_pos_dev; p.kept_count = a->kept_count_dev; p.colsum = a->colsum_dev;
+  p.choice = a->choice_dev; p.choice_stride = a->choice_stride; p.n_family = a->n_family;
+  for (int f = 0; f < a->n_family; ++f) {
+    p.fam_atoms[f] = a->family_atoms[f]; p.fam_r_l[f] = a->family_r_l[f]; p.fam_r_f[f] = a->family_r_f[f];
+  }
+  p.atoms = a->head_atoms_dev; p.r_l = a->head_r_l_dev; p.r_f = a->head_r_f_dev;
+  p.seg_off = a->seg_off_dev; p.seg_cap = a->seg_cap_dev;
+  p.kc = static_cast<uint4*>(a->kc_dev); p.vc = static_cast<uint4*>(a->vc_dev);
+  p.meta = a->meta_dev; p.score = a->score_dev; p.live = a->live_dev;
   dim3 grid((a->N + kCompactRows - 1) / kCompactRows, a->B * a->H);
   k2_compact<<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(p);
   cudaError_t e = cudaGetLastError();

@@ -247,22 +247,31 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
     if len(thresholds) > _lib.MAX_THRESHOLDS:
         raise ProfilerError(f"at most {_lib.MAX_THRESHOLDS} thresholds per profiling pass")
     F = len(family)
+    nT = len(thresholds)
     f32, f64, i32 = torch.float32, torch.float64, torch.int32
     classes = classes.to(torch.uint8).contiguous()
-    out = dict(
+    # per-head summary outputs share one device buffer -> one device->host copy
+    sections = [("recovery", G * F, f64), ("cosine", G * F, f64), ("lrr", G, f64),
+                ("gap", G, f64), ("total", 1, torch.int64), ("cost", G * F, i32),
+                ("kept_count", G, i32), ("choice", G * nT, torch.int8)]
+    offs, nbytes = {}, 0
+    for name, n, dtp in sections:
+        offs[name] = (nbytes, n, dtp)
+        nbytes += ((n * torch.empty(0, dtype=dtp).element_size() + 7) // 8) * 8
+    summary = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+
+    def view(buf, name):
+        o, n, dtp = offs[name]
+        return buf[o:o + n * torch.empty(0, dtype=dtp).element_size()].view(dtp)
+
+    out = {name: view(summary, name) for name, _, _ in sections}
+    out.update(
         lse=torch.empty(G, N, dtype=f32, device=dev),
         colsum=torch.empty(G, N, dtype=f64, device=dev),
         colsq=torch.empty(G, N, dtype=f64, device=dev),
         lastp=torch.empty(G, N, dtype=f32, device=dev),
         out_last=torch.empty(B, H, d, dtype=f32, device=dev),
-        recovery=torch.empty(G, F, dtype=f64, device=dev),
-        cost=torch.empty(G, F, dtype=i32, device=dev),
-        cosine=torch.empty(G, F, dtype=f64, device=dev),
-        choice=torch.empty(G, len(thresholds), dtype=torch.int8, device=dev),
         kept_pos=torch.empty(G, N, dtype=i32, device=dev),
-        kept_count=torch.empty(G, dtype=i32, device=dev),
-        lrr=torch.empty(G, dtype=f64, device=dev),
-        gap=torch.empty(G, dtype=f64, device=dev),
     )
     ws_bytes = lib.akv_profile_workspace_size(B, H, N, d)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
@@ -272,7 +281,7 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
     a.cls_dev, a.cls_ld = _ptr(classes), classes.shape[1]
     a.slope_dev, a.sink_dev = _ptr(slopes), _ptr(sinks)
     _family_arrays(family, a)
-    a.n_thresholds = len(thresholds)
+    a.n_thresholds = nT
     for i, t in enumerate(thresholds):
         a.thresholds[i] = t
     a.rows, a.criterion = rows, crit
@@ -285,31 +294,29 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
     stream = _stream()
     check(lib.akv_profile(C.byref(a), stream), ProfilerError)
 
-    # ragged arena plan (device prefix sum), then the one device->host read
+    # ragged arena plan (device prefix sum); the single device->host read of
+    # the session sizes the arena and brings the profile summary along
     seg_cap = torch.empty(G, dtype=i32, device=dev)
     seg_off = torch.empty(G, dtype=torch.int64, device=dev)
-    total = torch.empty(1, dtype=torch.int64, device=dev)
     check(lib.akv_plan_segments(G, _ptr(out["kept_count"]), int(max_new_tokens), _ptr(seg_cap),
-                                _ptr(seg_off), _ptr(total), stream))
-    host = {n: out[n].cpu() for n in ("recovery", "cost", "cosine", "choice", "kept_count", "lrr",
-                                      "gap")}
-    total_slots = int(total.item())
-    choice = host["choice"].numpy().astype(np.int64)
+                                _ptr(seg_off), _ptr(out["total"]), stream))
+    hsum = summary.cpu()
+    host = {name: view(hsum, name).numpy() for name, _, _ in sections}
+    total_slots = int(host["total"][0])
+    choice = host["choice"].reshape(G, nT).astype(np.int64)
     if (choice < 0).any():
         raise ProfilerError("no feasible policy met the threshold")
     res = ProfileResult(
-        family=family, thresholds=thresholds, recovery=host["recovery"].numpy(),
-        cost=host["cost"].numpy().astype(np.int64), cosine=host["cosine"].numpy(), choice=choice,
-        kept_count=host["kept_count"].numpy().astype(np.int64),
-        last_row_recovery=host["lrr"].numpy(), topk_gap=host["gap"].numpy())
+        family=family, thresholds=thresholds, recovery=host["recovery"].reshape(G, F),
+        cost=host["cost"].reshape(G, F).astype(np.int64), cosine=host["cosine"].reshape(G, F),
+        choice=choice, kept_count=host["kept_count"].astype(np.int64),
+        last_row_recovery=host["lrr"], topk_gap=host["gap"])
 
     cache = CompressedCache(B, H, d, q.dtype, N, int(max_new_tokens), dev)
     cache.profile_result = res
-    chosen = [family[c] for c in choice[:, 0]]
-    atoms = torch.tensor([p.bits for p in chosen], dtype=torch.uint8).to(dev, non_blocking=True)
-    cache.head_atoms = atoms
-    cache.head_r_l = torch.tensor([p.r_l for p in chosen], dtype=f64).to(dev, non_blocking=True)
-    cache.head_r_f = torch.tensor([p.r_f for p in chosen], dtype=f64).to(dev, non_blocking=True)
+    cache.head_atoms = torch.empty(G, dtype=torch.uint8, device=dev)
+    cache.head_r_l = torch.empty(G, dtype=f64, device=dev)
+    cache.head_r_f = torch.empty(G, dtype=f64, device=dev)
     cache.seg_cap, cache.seg_off = seg_cap, seg_off
     cache.max_cap = int(max(1, ((N + max_new_tokens + 7) // 8) * 8))
     cache.total_slots = max(total_slots, 1)
@@ -332,7 +339,13 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
     c.cls_dev, c.cls_ld = _ptr(classes), classes.shape[1]
     c.kept_pos_dev, c.kept_count_dev, c.colsum_dev = (_ptr(out["kept_pos"]),
                                                       _ptr(out["kept_count"]), _ptr(out["colsum"]))
-    c.head_atoms_dev, c.seg_off_dev, c.seg_cap_dev = _ptr(atoms), _ptr(seg_off), _ptr(seg_cap)
+    c.choice_dev, c.choice_stride = _ptr(out["choice"]), nT
+    c.n_family = F
+    for i, pol in enumerate(family):
+        c.family_atoms[i], c.family_r_l[i], c.family_r_f[i] = pol.bits, pol.r_l, pol.r_f
+    c.head_atoms_dev, c.head_r_l_dev, c.head_r_f_dev = (_ptr(cache.head_atoms),
+                                                        _ptr(cache.head_r_l), _ptr(cache.head_r_f))
+    c.seg_off_dev, c.seg_cap_dev = _ptr(seg_off), _ptr(seg_cap)
     c.kc_dev, c.vc_dev, c.meta_dev, c.score_dev = (_ptr(cache.kc), _ptr(cache.vc),
                                                    _ptr(cache.meta), _ptr(cache.score))
     c.live_dev = _ptr(cache.live_buf[0])
@@ -361,12 +374,13 @@ def _decode_args(cache: CompressedCache, dt: int) -> DecodeArgs:
     return a
 
 
-def decode_step_tensors(cache: CompressedCache, q, k, v, new_classes) -> torch.Tensor:
+def decode_step_tensors(cache: CompressedCache, q, k, v, new_classes, out=None) -> torch.Tensor:
     """One decode step for every head (Alg. 2 inner loop, engine.py:303-350):
     insert the new token's k/v, attend, update scores, evict.  q, k, v:
     CUDA tensors whose [B, H, :d] slices are the new token's rows (any
     head stride); new_classes: CUDA uint8 [B].  Returns the fp32 attention
-    output [B, H, d] (the cache's pending output buffer)."""
+    output [B, H, d]: ``out`` if given (contiguous fp32), else the cache's
+    pending-output buffer (overwritten by the next step)."""
     if cache.seq_len - cache.prompt_len >= cache.capacity_steps:
         raise EngineError(
             f"cache capacity of {cache.capacity_steps} decode steps exhausted; "
@@ -378,10 +392,12 @@ def decode_step_tensors(cache: CompressedCache, q, k, v, new_classes) -> torch.T
     a.new_cls_dev = _ptr(new_classes)
     a.live_in_dev = _ptr(cache.live_buf[cache._parity])
     a.live_out_dev = _ptr(cache.live_buf[cache._parity ^ 1])
+    dst = cache.out if out is None else out
+    a.out_dev = _ptr(dst)
     check(lib.akv_decode_step(C.byref(a), _stream()), EngineError)
     cache._parity ^= 1
     cache.seq_len += 1
-    return cache.out
+    return dst
 
 
 # ---------------------------------------------------------------------------
