@@ -46,6 +46,20 @@ def _peaks():
         return PEAKS_FALLBACK, "fallback"
 
 
+def _traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    capture summary (profiles/traffic.json, written by tools/ncu_summary.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        for name, v in t.items():
+            if name.endswith(kernel):
+                return v["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        pass
+    return None
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -61,7 +75,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -274,7 +288,7 @@ def bench_ours(args):
             "peak_kind": peak_kind,
             "unit": "GB/s",
             "frac": achieved / peaks.get("hbm_gbs"),
-            "traffic": None,
+            "traffic": _traffic("k3_decode_mma<128>"),
             "algorithmic_bytes_per_launch": avg_bytes,
             "avg_launch_us": launch_us,
         },
@@ -491,7 +505,7 @@ def bench_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--T", type=float, default=0.95)
