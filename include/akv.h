@@ -105,6 +105,8 @@ typedef struct akv_profile_args {
   int32_t* kept_count_dev;       /* [B*H] */
   double* last_row_recovery_dev; /* [B*H] A[N-1, kept].sum() */
   double* topk_gap_dev;          /* [B*H] min relative score gap at any frequent boundary */
+  uint64_t* topk_thr_key_dev;    /* [B*H] frequent top-k threshold of the primary choice: */
+  int32_t* topk_thr_pos_dev;     /*   position p is in the set iff (bits(colsum[p]), -p) >= (key, -pos) */
   void* workspace_dev;
   size_t workspace_bytes;
 } akv_profile_args;
@@ -125,6 +127,8 @@ typedef struct akv_compact_args {
   const int32_t* kept_count_dev; /* [B*H] */
   const double* colsum_dev;      /* [B*H,N] scores copied for FREQUENT heads */
   const int8_t* choice_dev;      /* [B*H,choice_stride] from akv_profile; column 0 is used */
+  const uint64_t* topk_thr_key_dev; /* [B*H] from akv_profile: marks the initial frequent set */
+  const int32_t* topk_thr_pos_dev;
   int32_t choice_stride;
   int32_t n_family;              /* the family akv_profile chose from */
   uint8_t family_atoms[AKV_MAX_FAMILY];

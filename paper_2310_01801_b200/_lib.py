@@ -37,8 +37,8 @@ class ProfileArgs(C.Structure):
         ("lse_dev", P), ("colsum_dev", P), ("colsq_dev", P), ("lastp_dev", P),
         ("out_last_dev", P), ("recovery_dev", P), ("cost_dev", P), ("cosine_dev", P),
         ("choice_dev", P), ("kept_pos_dev", P), ("kept_count_dev", P),
-        ("last_row_recovery_dev", P), ("topk_gap_dev", P),
-        ("workspace_dev", P), ("workspace_bytes", sz),
+        ("last_row_recovery_dev", P), ("topk_gap_dev", P), ("topk_thr_key_dev", P),
+        ("topk_thr_pos_dev", P), ("workspace_dev", P), ("workspace_bytes", sz),
     ]
 
 
@@ -47,7 +47,7 @@ class CompactArgs(C.Structure):
         ("B", i32), ("H", i32), ("N", i32), ("d", i32), ("dtype", i32),
         ("k_dev", P), ("v_dev", P), ("ld", i64), ("cls_dev", P), ("cls_ld", i64),
         ("kept_pos_dev", P), ("kept_count_dev", P), ("colsum_dev", P), ("choice_dev", P),
-        ("choice_stride", i32), ("n_family", i32), ("family_atoms", C.c_uint8 * MAX_FAMILY),
+        ("topk_thr_key_dev", P), ("topk_thr_pos_dev", P), ("choice_stride", i32), ("n_family", i32), ("family_atoms", C.c_uint8 * MAX_FAMILY),
         ("family_r_l", f64 * MAX_FAMILY), ("family_r_f", f64 * MAX_FAMILY),
         ("head_atoms_dev", P), ("head_r_l_dev", P), ("head_r_f_dev", P),
         ("seg_off_dev", P), ("seg_cap_dev", P), ("kc_dev", P), ("vc_dev", P),

@@ -26,6 +26,8 @@ struct CompactParams {
   const int32_t* kept_count;
   const double* colsum;
   const int8_t* choice;
+  const unsigned long long* thr_key;
+  const int32_t* thr_pos;
   int choice_stride;
   int n_family;
   uint8_t fam_atoms[AKV_MAX_FAMILY];
@@ -78,8 +80,11 @@ __global__ void __launch_bounds__(128) k2_compact(CompactParams p) {
   for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
     const int pos = kp[i0 + r];
     const int64_t slot = base + i0 + r;
-    p.meta[slot] = pos | ((int)p.cls[(size_t)b * p.cls_ld + pos] << kClsShift);
-    p.score[slot] = freq ? p.colsum[(size_t)g * p.N + pos] : 0.0;
+    const double sc = freq ? p.colsum[(size_t)g * p.N + pos] : 0.0;
+    const bool inF = freq && topk_selected((unsigned long long)__double_as_longlong(sc), pos,
+                                           p.thr_key[g], p.thr_pos[g]);
+    p.meta[slot] = pos | ((int)p.cls[(size_t)b * p.cls_ld + pos] << kClsShift) | (inF ? kInF : 0);
+    p.score[slot] = sc;
   }
 }
 
@@ -125,6 +130,10 @@ extern "C" int akv_compact(const akv_compact_args* a, void* stream) {
   p.cls = a->cls_dev; p.cls_ld = a->cls_ld;
   p.kept_pos = a->kept_pos_dev; p.kept_count = a->kept_count_dev; p.colsum = a->colsum_dev;
   p.choice = a->choice_dev; p.choice_stride = a->choice_stride; p.n_family = a->n_family;
+  p.thr_key = reinterpret_cast<const unsigned long long*>(a->topk_thr_key_dev);
+  p.thr_pos = a->topk_thr_pos_dev;
+  if (!p.thr_key || !p.thr_pos)
+    return set_error(AKV_ERR_INVALID, "akv_compact: topk threshold inputs are required");
   for (int f = 0; f < a->n_family; ++f) {
     p.fam_atoms[f] = a->family_atoms[f]; p.fam_r_l[f] = a->family_r_l[f]; p.fam_r_f[f] = a->family_r_f[f];
   }

@@ -54,8 +54,8 @@ namespace akv {
 constexpr int kStages = 3;
 constexpr int kPageBytes = 16384;  // per K (and per V) page
 constexpr int kMaxHeads = 2048;
-constexpr int kEpt = 16;
-constexpr int kSmemEvict = 64;  // evictions per head-step paired through shared memory  // register-resident candidates per thread in the epilogue
+constexpr int kEpr = 8;   // candidates per thread per batch in the epilogue passes
+constexpr int kSmemEvict = 64;  // evictions per head-step paired through shared memory
 
 struct DecParams {
   int B, H, G, prompt_len, pos;
@@ -176,111 +176,234 @@ __device__ __forceinline__ int head_of_page(const int* s_prefix, int G, long lon
   return lo;
 }
 
-// Keep rule + compaction for heads with more than NC*kEpt candidates:
-// every pass streams the head's slot metadata from L2.
+// Keep rule + compaction of one head (epilogue group CS).  Pass A streams
+// the head's slot metadata (and, for FREQUENT heads, the scores and this
+// step's logits) in coalesced batches of kEpr per thread: it applies the
+// score update (policies.py:355-357), gathers the statistics of the
+// incremental top-k (smallest key in the current frequent set F, largest
+// key outside it) and counts the slots that no atom keeps.  The common
+// outcomes are resolved from those statistics alone:
+//   * F still ranks above every other candidate and the budget grew by at
+//     most one -> F stays, plus the best outsider when the budget grew;
+//   * at most one slot leaves -> it is refilled from the segment tail.
+// Otherwise a crossing repair re-ranks only the candidates between the two
+// extremes (the rest of the order is fixed), falling back to the exact
+// radix select, and a general compaction pass pairs holes with donors.
 template <typename CS>
-__device__ void policy_global(const DecParams& p, const HeadCtx& hc, float lse, int* hist,
-                              int* red_i, int rv) {
+__device__ void policy_v3(const DecParams& p, const HeadCtx& hc, float lse, int* hist, int* red_i,
+                          int rv) {
   constexpr int NC = CS::kThreads, NW = CS::kWarps;
   const int tid = CS::tid(), lane = tid & 31, warp = tid >> 5;
   const int g = hc.g, L = hc.L, n = hc.n;
   const int cur = p.pos + 1;
   double* score = p.score + hc.base;
   int32_t* meta = p.meta + hc.base;
+  const float* lg = p.logit + hc.base;
   const uint8_t atoms = hc.atoms;
   const bool freq = hc.freq;
-  __shared__ int s_fast;
-  __shared__ int s_add;  // slot joining the frequent set on the fast path (-1: none)
-  __shared__ unsigned long long s_k[2][NW];
-  __shared__ int s_i[4][NW];
-  if (freq) {
-    // score update (policies.py:355-357; score[new] = 0 was written by the
-    // inserting consumer) fused with the fast-path statistics: the smallest
-    // key of the current frequent set F and the largest key outside it.
-    const float* lg = p.logit + hc.base;
-    unsigned long long minF_k = ~0ull, maxN_k = 0ull;
-    int minF_p = -1, maxN_p = 0x7fffffff, maxN_slot = -1, cntF = 0, anyN = 0;
-    for (int j = tid; j < n; j += NC) {
-      double s = __ldcg(score + j);
-      if (j < L) {
-        s += (double)expf(__ldcg(lg + j) - lse);
-        score[j] = s;
-      }
-      const int m = __ldcg(meta + j);
-      const unsigned long long key = (unsigned long long)__double_as_longlong(s);
-      const int ps = meta_pos(m);
-      if (m & kInF) {
-        ++cntF;
-        if (key < minF_k || (key == minF_k && ps > minF_p)) { minF_k = key; minF_p = ps; }
-      } else if (!anyN || key > maxN_k || (key == maxN_k && ps < maxN_p)) {
-        maxN_k = key; maxN_p = ps; maxN_slot = j; anyN = 1;
-      }
+  const int window_start = cur - budget(p.r_l[g], p.prompt_len);
+  auto class_keep = [&](int m) -> bool {
+    const int cl = meta_cls(m), ps = meta_pos(m);
+    return ((atoms & AKV_ATOM_SPECIAL) && cl == AKV_CLS_SPECIAL) ||
+           ((atoms & AKV_ATOM_PUNCT) && cl == AKV_CLS_PUNCT) ||
+           ((atoms & AKV_ATOM_LOCAL) && ps >= window_start);
+  };
+  // key order: larger score first, then lower position (policies.py:238-240)
+  auto above = [](unsigned long long ka, int pa, unsigned long long kb, int pb) {
+    return ka > kb || (ka == kb && pa < pb);
+  };
+
+  // ---------------- pass A ----------------
+  unsigned long long minF_k = ~0ull, maxN_k = 0ull;
+  int minF_p = -1, maxN_p = 0x7fffffff, maxN_slot = -1, maxN_ck = 0, anyN = 0, cntF = 0;
+  int nk_cnt = 0, nk_min = 0x7fffffff, nk_max = -1, new_ck = 0;
+  for (int b0 = 0; b0 < n; b0 += NC * kEpr) {
+    int mv[kEpr];
+    double sv[kEpr];
+    float lv[kEpr];
+#pragma unroll
+    for (int i = 0; i < kEpr; ++i) {
+      const int j = b0 + i * NC + tid;
+      mv[i] = j < n ? __ldcg(meta + j) : 0;
+      sv[i] = (freq && j < n) ? __ldcg(score + j) : 0.0;
+      lv[i] = (freq && j < L) ? __ldcg(lg + j) : 0.f;
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int i = 0; i < kEpr; ++i) {
+      const int j = b0 + i * NC + tid;
+      if (j >= n) continue;
+      if (freq && j < L) {
+        sv[i] += (double)expf(lv[i] - lse);
+        score[j] = sv[i];
+      }
+      const bool ck = class_keep(mv[i]);
+      const bool inF = freq && (mv[i] & kInF);
+      if (j == L) new_ck = ck;
+      else if (!ck && !inF) { ++nk_cnt; nk_min = min(nk_min, j); nk_max = max(nk_max, j); }
+      if (freq) {
+        const unsigned long long key = (unsigned long long)__double_as_longlong(sv[i]);
+        const int ps = meta_pos(mv[i]);
+        if (inF) {
+          ++cntF;
+          if (!above(key, ps, minF_k, minF_p) && (key != minF_k || ps != minF_p)) { minF_k = key; minF_p = ps; }
+        } else if (!anyN || above(key, ps, maxN_k, maxN_p)) {
+          maxN_k = key; maxN_p = ps; maxN_slot = j; maxN_ck = ck; anyN = 1;
+        }
+      }
+    }
+  }
+  // group reductions
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nk_cnt += __shfl_xor_sync(0xffffffffu, nk_cnt, o);
+    nk_min = min(nk_min, __shfl_xor_sync(0xffffffffu, nk_min, o));
+    nk_max = max(nk_max, __shfl_xor_sync(0xffffffffu, nk_max, o));
+    new_ck |= __shfl_xor_sync(0xffffffffu, new_ck, o);
+    if (freq) {
       const unsigned long long ok = __shfl_xor_sync(0xffffffffu, minF_k, o);
       const int op = __shfl_xor_sync(0xffffffffu, minF_p, o);
-      if (ok < minF_k || (ok == minF_k && op > minF_p)) { minF_k = ok; minF_p = op; }
+      if (above(minF_k, minF_p, ok, op)) { minF_k = ok; minF_p = op; }
       const unsigned long long nk = __shfl_xor_sync(0xffffffffu, maxN_k, o);
       const int np_ = __shfl_xor_sync(0xffffffffu, maxN_p, o);
       const int ns = __shfl_xor_sync(0xffffffffu, maxN_slot, o);
+      const int nc = __shfl_xor_sync(0xffffffffu, maxN_ck, o);
       const int na = __shfl_xor_sync(0xffffffffu, anyN, o);
-      if (na && (!anyN || nk > maxN_k || (nk == maxN_k && np_ < maxN_p))) {
-        maxN_k = nk; maxN_p = np_; maxN_slot = ns; anyN = 1;
+      if (na && (!anyN || above(nk, np_, maxN_k, maxN_p))) {
+        maxN_k = nk; maxN_p = np_; maxN_slot = ns; maxN_ck = nc; anyN = 1;
       }
       cntF += __shfl_xor_sync(0xffffffffu, cntF, o);
     }
-    CS::sync();
-    if (lane == 0) {
-      s_k[0][warp] = minF_k; s_i[0][warp] = minF_p;
-      s_k[1][warp] = maxN_k; s_i[1][warp] = maxN_p;
-      s_i[2][warp] = anyN ? maxN_slot : -1;
-      s_i[3][warp] = cntF;
-    }
-    CS::sync();
-    if (tid == 0) {
-      unsigned long long mf = ~0ull, mn = 0ull;
-      int mfp = -1, mnp = 0x7fffffff, mns = -1, cf = 0;
-      bool an = false;
-      for (int w = 0; w < NW; ++w) {
-        cf += s_i[3][w];
-        if (s_k[0][w] < mf || (s_k[0][w] == mf && s_i[0][w] > mfp)) { mf = s_k[0][w]; mfp = s_i[0][w]; }
-        if (s_i[2][w] >= 0 && (!an || s_k[1][w] > mn || (s_k[1][w] == mn && s_i[1][w] < mnp))) {
-          mn = s_k[1][w]; mnp = s_i[1][w]; mns = s_i[2][w]; an = true;
-        }
+  }
+  __shared__ unsigned long long s_k[2][NW];
+  __shared__ int s_i[9][NW];
+  __shared__ int s_mode, s_add, s_nkeep, s_x, s_donor, s_cnt;
+  __shared__ unsigned long long s_mf_k, s_mn_k;
+  __shared__ int s_mf_p, s_mn_p, s_kb;
+  CS::sync();
+  if (lane == 0) {
+    s_k[0][warp] = minF_k; s_i[0][warp] = minF_p;
+    s_k[1][warp] = maxN_k; s_i[1][warp] = maxN_p;
+    s_i[2][warp] = anyN ? maxN_slot : -1; s_i[3][warp] = maxN_ck;
+    s_i[4][warp] = cntF; s_i[5][warp] = nk_cnt; s_i[6][warp] = nk_min; s_i[7][warp] = nk_max;
+    s_i[8][warp] = new_ck;
+  }
+  CS::sync();
+  if (tid == 0) {
+    unsigned long long mf = ~0ull, mn = 0ull;
+    int mfp = -1, mnp = 0x7fffffff, mns = -1, mnc = 0, cf = 0, ec = 0, emin = 0x7fffffff, emax = -1, nck = 0;
+    bool an = false;
+    for (int w = 0; w < NW; ++w) {
+      cf += s_i[4][w]; ec += s_i[5][w];
+      emin = min(emin, s_i[6][w]); emax = max(emax, s_i[7][w]); nck |= s_i[8][w];
+      if (above(mf, mfp, s_k[0][w], s_i[0][w])) { mf = s_k[0][w]; mfp = s_i[0][w]; }
+      if (s_i[2][w] >= 0 && (!an || above(s_k[1][w], s_i[1][w], mn, mnp))) {
+        mn = s_k[1][w]; mnp = s_i[1][w]; mns = s_i[2][w]; mnc = s_i[3][w]; an = true;
       }
-      const int kb = budget(p.r_f[g], cur);
-      int f = 0, add = -1;
-      if (kb >= n) {
-        f = 2;  // every candidate is selected
-      } else if (cf > 0 && (kb == cf || kb == cf + 1)) {
-        // F is still the top-|F| set iff all of F outranks everything else
-        const bool separated = !an || mn < mf || (mn == mf && mnp > mfp);
-        if (separated) {
-          f = 1;
-          if (kb == cf + 1) add = mns;
-        }
-      }
-      s_fast = f;
-      s_add = add;
     }
-    CS::sync();
-    if (s_fast == 1) {
+    // mode: 0 resolved from statistics, 1 crossing repair, 2 radix select, 3 select all
+    int mode = 0, add = -1;
+    const int kb = freq ? budget(p.r_f[g], cur) : 0;
+    if (freq) {
+      if (kb >= n) mode = 3;
+      else if (cf == 0) mode = 2;
+      else if (!an || above(mf, mfp, mn, mnp)) {  // F separated from the rest
+        if (kb == cf) mode = 0;
+        else if (kb == cf + 1) { mode = 0; add = mns; }
+        else mode = 2;
+      } else {
+        mode = 1;
+      }
+    }
+    int nkeep = -1, x = -1, donor = -1;
+    if (mode == 0) {
+      // slots leaving: old slots no atom keeps, minus the joining outsider
+      int e = ec;
+      int a0 = emin, a1 = emax;
+      if (add >= 0 && add != L && !mnc) {
+        --e;
+        if (add == a0) a0 = a1; else if (add == a1) a1 = a0;
+      }
+      const bool new_kept = nck || add == L;
+      if (e == 0) {
+        nkeep = new_kept ? n : n - 1;
+      } else if (e == 1) {
+        x = a0;
+        if (new_kept) { nkeep = n - 1; donor = n - 1; }
+        else { nkeep = n - 2; donor = (x == n - 2) ? -1 : n - 2; }
+      }
+    }
+    s_mode = mode; s_add = add; s_nkeep = nkeep; s_x = x; s_donor = donor;
+    s_mf_k = mf; s_mf_p = mfp; s_mn_k = mn; s_mn_p = mnp; s_kb = kb;
+    s_cnt = 0;
+  }
+  CS::sync();
+  int mode = s_mode;
+  if (freq) {
+    if (mode == 0) {
       if (tid == 0 && s_add >= 0) meta[s_add] = __ldcg(meta + s_add) | kInF;
-    } else {
-      unsigned long long thr_key = 0ull;
-      int thr_pos = 0x7fffffff;
-      if (s_fast == 0) {
-        if (p.trace && tid == 0) atomicAdd(&p.trace[blockIdx.x * 8 + 7], 1ull);  // fallbacks
-        const int kb = budget(p.r_f[g], cur);
-        auto get = [&](int i, unsigned long long* key, int* pos) {
-          *key = (unsigned long long)__double_as_longlong(__ldcg(score + i));
-          *pos = meta_pos(__ldcg(meta + i));
-        };
-        block_topk_threshold<CS>(n, kb, get, hist, red_i, &thr_key, &thr_pos);
+    } else if (mode == 3) {  // every candidate is in the frequent set
+      for (int j = tid; j < n; j += NC) {
+        const int m = __ldcg(meta + j);
+        if (!(m & kInF)) meta[j] = m | kInF;
       }
+    } else if (mode == 1) {
+      // crossing repair: F members above the best outsider stay, outsiders
+      // below the weakest F member stay out; re-rank the band between them
+      constexpr int kBand = 128;
+      __shared__ unsigned long long s_bk[kBand];
+      __shared__ int s_bp[kBand], s_bs[kBand];
+      __shared__ int s_above;
+      if (tid == 0) s_above = 0;
       CS::sync();
-      // rewrite the inF flags from the exact threshold
+      const unsigned long long mf = s_mf_k, mn = s_mn_k;
+      const int mfp = s_mf_p, mnp = s_mn_p;
+      int my_above = 0;
+      for (int b0 = 0; b0 < n; b0 += NC * kEpr) {
+        int mv[kEpr];
+        double sv[kEpr];
+#pragma unroll
+        for (int i = 0; i < kEpr; ++i) {
+          const int j = b0 + i * NC + tid;
+          mv[i] = j < n ? __ldcg(meta + j) : 0;
+          sv[i] = j < n ? __ldcg(score + j) : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < kEpr; ++i) {
+          const int j = b0 + i * NC + tid;
+          if (j >= n) continue;
+          const unsigned long long key = (unsigned long long)__double_as_longlong(sv[i]);
+          const int ps = meta_pos(mv[i]);
+          if (above(key, ps, mn, mnp)) { my_above += (mv[i] & kInF) ? 1 : 0; continue; }
+          if (above(mf, mfp, key, ps)) continue;  // strictly below the weakest F member
+          const int at = atomicAdd(&s_cnt, 1);
+          if (at < kBand) { s_bk[at] = key; s_bp[at] = ps; s_bs[at] = j; }
+        }
+      }
+      my_above = block_sum<int, CS>(my_above, red_i);
+      const int band = s_cnt;
+      const int need = s_kb - my_above;
+      if (band > kBand || need < 0 || need > band) {
+        mode = 2;
+      } else {
+        for (int c = tid; c < band; c += NC) {
+          int rank = 0;
+          for (int o = 0; o < band; ++o) rank += above(s_bk[o], s_bp[o], s_bk[c], s_bp[c]);
+          const int j = s_bs[c];
+          const int m = __ldcg(meta + j);
+          const int nm = rank < need ? (m | kInF) : (m & ~kInF);
+          if (nm != m) meta[j] = nm;
+        }
+      }
+    }
+    if (mode == 2) {  // exact radix select over all candidates
+      if (p.trace && tid == 0) atomicAdd(&p.trace[blockIdx.x * 8 + 7], 1ull);
+      unsigned long long thr_key;
+      int thr_pos;
+      auto get = [&](int i, unsigned long long* key, int* pos) {
+        *key = (unsigned long long)__double_as_longlong(__ldcg(score + i));
+        *pos = meta_pos(__ldcg(meta + i));
+      };
+      block_topk_threshold<CS>(n, s_kb, get, hist, red_i, &thr_key, &thr_pos);
       for (int j = tid; j < n; j += NC) {
         const int m = __ldcg(meta + j);
         const bool sel = topk_selected((unsigned long long)__double_as_longlong(__ldcg(score + j)),
@@ -291,245 +414,82 @@ __device__ void policy_global(const DecParams& p, const HeadCtx& hc, float lse, 
     }
     CS::sync();
   }
-  const int window_start = cur - budget(p.r_l[g], p.prompt_len);
-  auto keep = [&](int j) -> bool {
-    const int m = __ldcg(meta + j);
-    const int cl = meta_cls(m), ps = meta_pos(m);
-    return ((atoms & AKV_ATOM_SPECIAL) && cl == AKV_CLS_SPECIAL) ||
-           ((atoms & AKV_ATOM_PUNCT) && cl == AKV_CLS_PUNCT) ||
-           ((atoms & AKV_ATOM_LOCAL) && ps >= window_start) || (freq && (m & kInF));
-  };
-  // count kept, then pair holes (evicted slots below n') with donors (kept
-  // slots at or above n'), both in slot order
-  const int per = (n + NC - 1) / NC;
-  const int lo = min(n, tid * per), hi = min(n, lo + per);
-  int nk = 0;
-  for (int j = lo; j < hi; ++j) nk += keep(j);
-  const int n_keep = block_sum<int, CS>(nk, red_i);
-  if (n_keep < n) {
-    int holes = 0, donors = 0;
-    for (int j = lo; j < hi; ++j) {
-      const bool k = keep(j);
-      holes += (j < n_keep && !k);
-      donors += (j >= n_keep && k);
-    }
-    int n_holes, n_donors;
-    int hole_off = block_exclusive_scan<CS>(holes, red_i, &n_holes);
-    int donor_off = block_exclusive_scan<CS>(donors, red_i, &n_donors);
-    int* hole_list = reinterpret_cast<int*>(p.logit + hc.base);  // logits are consumed
-    int* donor_list = hole_list + n_holes;
-    for (int j = lo; j < hi; ++j) {
-      const bool k = keep(j);
-      if (j < n_keep && !k) hole_list[hole_off++] = j;
-      if (j >= n_keep && k) donor_list[donor_off++] = j;
-    }
-    CS::sync();
-    uint4* kw = static_cast<uint4*>(p.kc) + hc.base * rv;
-    uint4* vw = static_cast<uint4*>(p.vc) + hc.base * rv;
-    for (int r = warp; r < n_holes; r += NW) {
-      const int dst = __ldcg(hole_list + r), src = __ldcg(donor_list + r);
+  uint4* kw = static_cast<uint4*>(p.kc) + hc.base * rv;
+  uint4* vw = static_cast<uint4*>(p.vc) + hc.base * rv;
+  int n_keep;
+  if (mode == 0 && s_nkeep >= 0) {
+    // at most one hole, refilled from the tail
+    n_keep = s_nkeep;
+    const int x = s_x, src = s_donor;
+    if (x >= 0 && src >= 0 && warp == 0) {
       for (int v = lane; v < rv; v += 32) {
-        st_v4(kw + (size_t)dst * rv + v, ld_cg_v4(kw + (size_t)src * rv + v));
-        st_v4(vw + (size_t)dst * rv + v, ld_cg_v4(vw + (size_t)src * rv + v));
+        st_v4(kw + (size_t)x * rv + v, ld_cg_v4(kw + (size_t)src * rv + v));
+        st_v4(vw + (size_t)x * rv + v, ld_cg_v4(vw + (size_t)src * rv + v));
       }
       if (lane == 0) {
-        meta[dst] = __ldcg(meta + src);
-        score[dst] = __ldcg(score + src);
+        meta[x] = __ldcg(meta + src);
+        if (freq) score[x] = __ldcg(score + src);
       }
     }
-  }
-  if (tid == 0) {
-    p.live_out[g] = n_keep;
-    if (p.evicted) p.evicted[g] = n - n_keep;
-    p.counter[g] = 0;
-  }
-  CS::sync();
-}
-
-
-// Keep rule + compaction with each thread's contiguous slice of the
-// candidates (<= kEpt) held in registers: one load pass, then reductions
-// and scans on registers, one write-back pass.
-template <typename CS>
-__device__ void policy_regs(const DecParams& p, const HeadCtx& hc, float lse, int* hist,
-                            int* red_i, int rv) {
-  constexpr int NC = CS::kThreads, NW = CS::kWarps;
-  const int tid = CS::tid(), lane = tid & 31, warp = tid >> 5;
-  const int g = hc.g, L = hc.L, n = hc.n;
-  const int cur = p.pos + 1;
-  double* score = p.score + hc.base;
-  int32_t* meta = p.meta + hc.base;
-  const uint8_t atoms = hc.atoms;
-  const bool freq = hc.freq;
-  const int per = (n + NC - 1) / NC;
-  const int lo = min(n, tid * per), hi = min(n, lo + per);
-  int mt[kEpt];
-  double sc[kEpt];
+  } else if (mode == 3) {
+    n_keep = n;
+  } else {
+    // general compaction: count, then pair holes (dropped slots below n')
+    // with donors (kept slots at or above n'); any pairing is valid
+    auto keep = [&](int m) { return class_keep(m) || (freq && (m & kInF)); };
+    int nk = 0;
+    for (int b0 = 0; b0 < n; b0 += NC * kEpr) {
+      int mv[kEpr];
 #pragma unroll
-  for (int i = 0; i < kEpt; ++i) {
-    const int j = lo + i;
-    mt[i] = (j < hi) ? __ldcg(meta + j) : 0;
-    sc[i] = (freq && j < hi) ? __ldcg(score + j) : 0.0;
-  }
-  __shared__ int s_fast, s_add;
-  __shared__ unsigned long long s_k[2][NW];
-  __shared__ int s_i[4][NW];
-  if (freq) {
-    // score update (policies.py:355-357; score[new] = 0 was written by the
-    // inserting consumer) and the fast-path statistics: the smallest key of
-    // the current frequent set F and the largest key outside it
-    const float* lg = p.logit + hc.base;
-    float lv[kEpt];
-#pragma unroll
-    for (int i = 0; i < kEpt; ++i) lv[i] = (lo + i < hi && lo + i < L) ? __ldcg(lg + lo + i) : 0.f;
-    unsigned long long minF_k = ~0ull, maxN_k = 0ull;
-    int minF_p = -1, maxN_p = 0x7fffffff, maxN_slot = -1, cntF = 0, anyN = 0;
-#pragma unroll
-    for (int i = 0; i < kEpt; ++i) {
-      const int j = lo + i;
-      if (j >= hi) continue;
-      if (j < L) {
-        sc[i] += (double)expf(lv[i] - lse);
-        score[j] = sc[i];
+      for (int i = 0; i < kEpr; ++i) {
+        const int j = b0 + i * NC + tid;
+        mv[i] = j < n ? __ldcg(meta + j) : 0;
       }
-      const unsigned long long key = (unsigned long long)__double_as_longlong(sc[i]);
-      const int ps = meta_pos(mt[i]);
-      if (mt[i] & kInF) {
-        ++cntF;
-        if (key < minF_k || (key == minF_k && ps > minF_p)) { minF_k = key; minF_p = ps; }
-      } else if (!anyN || key > maxN_k || (key == maxN_k && ps < maxN_p)) {
-        maxN_k = key; maxN_p = ps; maxN_slot = j; anyN = 1;
-      }
-    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, minF_k, o);
-      const int op = __shfl_xor_sync(0xffffffffu, minF_p, o);
-      if (ok < minF_k || (ok == minF_k && op > minF_p)) { minF_k = ok; minF_p = op; }
-      const unsigned long long nk = __shfl_xor_sync(0xffffffffu, maxN_k, o);
-      const int np_ = __shfl_xor_sync(0xffffffffu, maxN_p, o);
-      const int ns = __shfl_xor_sync(0xffffffffu, maxN_slot, o);
-      const int na = __shfl_xor_sync(0xffffffffu, anyN, o);
-      if (na && (!anyN || nk > maxN_k || (nk == maxN_k && np_ < maxN_p))) {
-        maxN_k = nk; maxN_p = np_; maxN_slot = ns; anyN = 1;
-      }
-      cntF += __shfl_xor_sync(0xffffffffu, cntF, o);
+      for (int i = 0; i < kEpr; ++i) nk += (b0 + i * NC + tid < n) && keep(mv[i]);
     }
-    CS::sync();
-    if (lane == 0) {
-      s_k[0][warp] = minF_k; s_i[0][warp] = minF_p;
-      s_k[1][warp] = maxN_k; s_i[1][warp] = maxN_p;
-      s_i[2][warp] = anyN ? maxN_slot : -1;
-      s_i[3][warp] = cntF;
-    }
-    CS::sync();
-    if (tid == 0) {
-      unsigned long long mf = ~0ull, mn = 0ull;
-      int mfp = -1, mnp = 0x7fffffff, mns = -1, cf = 0;
-      bool an = false;
-      for (int w = 0; w < NW; ++w) {
-        cf += s_i[3][w];
-        if (s_k[0][w] < mf || (s_k[0][w] == mf && s_i[0][w] > mfp)) { mf = s_k[0][w]; mfp = s_i[0][w]; }
-        if (s_i[2][w] >= 0 && (!an || s_k[1][w] > mn || (s_k[1][w] == mn && s_i[1][w] < mnp))) {
-          mn = s_k[1][w]; mnp = s_i[1][w]; mns = s_i[2][w]; an = true;
+    n_keep = block_sum<int, CS>(nk, red_i);
+    if (n_keep < n) {
+      __shared__ int s_hole[kSmemEvict], s_don[kSmemEvict];
+      __shared__ int s_nh, s_nd;
+      if (tid == 0) { s_nh = 0; s_nd = 0; }
+      CS::sync();
+      int* gl_hole = reinterpret_cast<int*>(p.logit + hc.base);  // logits are consumed
+      const int cap_g = n / 2;
+      for (int b0 = 0; b0 < n; b0 += NC * kEpr) {
+        int mv[kEpr];
+#pragma unroll
+        for (int i = 0; i < kEpr; ++i) {
+          const int j = b0 + i * NC + tid;
+          mv[i] = j < n ? __ldcg(meta + j) : 0;
+        }
+#pragma unroll
+        for (int i = 0; i < kEpr; ++i) {
+          const int j = b0 + i * NC + tid;
+          if (j >= n) continue;
+          const bool k = keep(mv[i]);
+          if (j < n_keep && !k) {
+            const int at = atomicAdd(&s_nh, 1);
+            if (at < kSmemEvict) s_hole[at] = j; else gl_hole[at] = j;
+          } else if (j >= n_keep && k) {
+            const int at = atomicAdd(&s_nd, 1);
+            if (at < kSmemEvict) s_don[at] = j; else gl_hole[cap_g + at] = j;
+          }
         }
       }
-      const int kb = budget(p.r_f[g], cur);
-      int f = 0, add = -1;
-      if (kb >= n) {
-        f = 2;  // every candidate is selected
-      } else if (cf > 0 && (kb == cf || kb == cf + 1)) {
-        // F is still the top-|F| set iff all of F outranks everything else
-        const bool separated = !an || mn < mf || (mn == mf && mnp > mfp);
-        if (separated) {
-          f = 1;
-          if (kb == cf + 1) add = mns;
+      CS::sync();
+      const int nh = s_nh;
+      for (int r = warp; r < nh; r += NW) {
+        const int dst = r < kSmemEvict ? s_hole[r] : __ldcg(gl_hole + r);
+        const int src = r < kSmemEvict ? s_don[r] : __ldcg(gl_hole + cap_g + r);
+        for (int v = lane; v < rv; v += 32) {
+          st_v4(kw + (size_t)dst * rv + v, ld_cg_v4(kw + (size_t)src * rv + v));
+          st_v4(vw + (size_t)dst * rv + v, ld_cg_v4(vw + (size_t)src * rv + v));
         }
-      }
-      s_fast = f;
-      s_add = add;
-    }
-    CS::sync();
-    const int fast = s_fast, add = s_add;
-    unsigned long long thr_key = 0ull;
-    int thr_pos = 0x7fffffff;
-    if (fast == 0) {  // exact radix select over the registers (rare)
-      if (p.trace && tid == 0) atomicAdd(&p.trace[blockIdx.x * 8 + 7], 1ull);
-      unsigned long long kk[kEpt];
-      int pp[kEpt];
-#pragma unroll
-      for (int i = 0; i < kEpt; ++i) {
-        kk[i] = (unsigned long long)__double_as_longlong(sc[i]);
-        pp[i] = meta_pos(mt[i]);
-      }
-      regs_topk_threshold<CS, kEpt>(n, budget(p.r_f[g], cur), kk, pp, hi - lo, hist, &thr_key,
-                                    &thr_pos);
-    }
-#pragma unroll
-    for (int i = 0; i < kEpt; ++i) {
-      const int j = lo + i;
-      if (j >= hi) continue;
-      int nm = mt[i];
-      if (fast == 1) {
-        if (j == add) nm |= kInF;
-      } else {
-        const bool sel = topk_selected((unsigned long long)__double_as_longlong(sc[i]),
-                                       meta_pos(mt[i]), thr_key, thr_pos);
-        nm = sel ? (nm | kInF) : (nm & ~kInF);
-      }
-      if (nm != mt[i]) { mt[i] = nm; meta[j] = nm; }
-    }
-  }
-  const int window_start = cur - budget(p.r_l[g], p.prompt_len);
-  bool kp[kEpt];
-  int nk = 0;
-#pragma unroll
-  for (int i = 0; i < kEpt; ++i) {
-    const int cl = meta_cls(mt[i]), ps = meta_pos(mt[i]);
-    kp[i] = (lo + i < hi) &&
-            (((atoms & AKV_ATOM_SPECIAL) && cl == AKV_CLS_SPECIAL) ||
-             ((atoms & AKV_ATOM_PUNCT) && cl == AKV_CLS_PUNCT) ||
-             ((atoms & AKV_ATOM_LOCAL) && ps >= window_start) || (freq && (mt[i] & kInF)));
-    nk += kp[i];
-  }
-  const int n_keep = block_sum<int, CS>(nk, red_i);
-  if (n_keep < n) {
-    int holes = 0, donors = 0;
-#pragma unroll
-    for (int i = 0; i < kEpt; ++i) {
-      const int j = lo + i;
-      if (j >= hi) continue;
-      holes += (j < n_keep && !kp[i]);
-      donors += (j >= n_keep && kp[i]);
-    }
-    int n_holes, n_donors;
-    int hole_off = block_exclusive_scan<CS>(holes, red_i, &n_holes);
-    int donor_off = block_exclusive_scan<CS>(donors, red_i, &n_donors);
-    // pairing lists: shared memory for the usual handful of evictions,
-    // the (consumed) logit scratch of the head otherwise
-    __shared__ int s_lists[2 * kSmemEvict];
-    int* hole_list = n_holes <= kSmemEvict ? s_lists : reinterpret_cast<int*>(p.logit + hc.base);
-    int* donor_list = n_holes <= kSmemEvict ? s_lists + kSmemEvict : hole_list + n_holes;
-#pragma unroll
-    for (int i = 0; i < kEpt; ++i) {
-      const int j = lo + i;
-      if (j >= hi) continue;
-      if (j < n_keep && !kp[i]) hole_list[hole_off++] = j;
-      if (j >= n_keep && kp[i]) donor_list[donor_off++] = j;
-    }
-    CS::sync();
-    uint4* kw = static_cast<uint4*>(p.kc) + hc.base * rv;
-    uint4* vw = static_cast<uint4*>(p.vc) + hc.base * rv;
-    for (int r = warp; r < n_holes; r += NW) {
-      const int dst = n_holes <= kSmemEvict ? hole_list[r] : __ldcg(hole_list + r);
-      const int src = n_holes <= kSmemEvict ? donor_list[r] : __ldcg(donor_list + r);
-      for (int v = lane; v < rv; v += 32) {
-        st_v4(kw + (size_t)dst * rv + v, ld_cg_v4(kw + (size_t)src * rv + v));
-        st_v4(vw + (size_t)dst * rv + v, ld_cg_v4(vw + (size_t)src * rv + v));
-      }
-      if (lane == 0) {
-        meta[dst] = __ldcg(meta + src);
-        score[dst] = __ldcg(score + src);
+        if (lane == 0) {
+          meta[dst] = __ldcg(meta + src);
+          if (freq) score[dst] = __ldcg(score + src);
+        }
       }
     }
   }
@@ -606,10 +566,7 @@ __device__ void head_epilogue(const DecParams& p, const HeadCtx& hc, int nparts,
     return;
   }
   const float lse = gM + logf(gl);
-  if ((n + NC - 1) / NC <= kEpt)
-    policy_regs<CS>(p, hc, lse, hist, red_i, rv);
-  else
-    policy_global<CS>(p, hc, lse, hist, red_i, rv);
+  policy_v3<CS>(p, hc, lse, hist, red_i, rv);
 }
 
 // Publish a CTA's partial (max, sum, o[D]) for head g from NWC per-warp

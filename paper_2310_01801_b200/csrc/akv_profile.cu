@@ -280,6 +280,8 @@ struct PolicyParams {
   int32_t* kept_count;
   double* last_row_recovery;
   double* topk_gap;
+  unsigned long long* thr_key;
+  int32_t* thr_pos;
 };
 
 constexpr int kPolicyThreads = 512;
@@ -403,6 +405,10 @@ __global__ void __launch_bounds__(kPolicyThreads) k1_policy(PolicyParams p) {
   if (threadIdx.x == 0) {
     p.kept_count[g] = f0 >= 0 ? total : 0;
     p.last_row_recovery[g] = f0 >= 0 ? lr : 0.0;
+    // initial frequent set of the chosen policy (decode's incremental top-k)
+    const bool fr = f0 >= 0 && (p.atoms[f0] & AKV_ATOM_FREQUENT) && !(p.atoms[f0] & AKV_ATOM_FULL);
+    p.thr_key[g] = fr ? s_thr_key[f0] : ~0ull;
+    p.thr_pos[g] = fr ? s_thr_pos[f0] : -1;
   }
   // pending output A[N-1] @ V = sum of the per-key-tile partials
   for (int c = threadIdx.x; c < p.d; c += blockDim.x) {
@@ -505,6 +511,10 @@ extern "C" int akv_profile(const akv_profile_args* a, void* stream) {
   pol.cosine = a->cosine_dev; pol.choice = a->choice_dev; pol.kept_pos = a->kept_pos_dev;
   pol.kept_count = a->kept_count_dev; pol.last_row_recovery = a->last_row_recovery_dev;
   pol.topk_gap = a->topk_gap_dev;
+  pol.thr_key = reinterpret_cast<unsigned long long*>(a->topk_thr_key_dev);
+  pol.thr_pos = a->topk_thr_pos_dev;
+  if (!pol.thr_key || !pol.thr_pos)
+    return set_error(AKV_ERR_INVALID, "akv_profile: topk threshold outputs are required");
   k1_policy<<<G, kPolicyThreads, 0, st>>>(pol);
   e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(AKV_ERR_CUDA, "akv_profile policy: %s", cudaGetErrorString(e));

@@ -266,6 +266,8 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
 
     out = {name: view(summary, name) for name, _, _ in sections}
     out.update(
+        thr_key=torch.empty(G, dtype=torch.int64, device=dev),
+        thr_pos=torch.empty(G, dtype=i32, device=dev),
         lse=torch.empty(G, N, dtype=f32, device=dev),
         colsum=torch.empty(G, N, dtype=f64, device=dev),
         colsq=torch.empty(G, N, dtype=f64, device=dev),
@@ -290,6 +292,7 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
      a.last_row_recovery_dev, a.topk_gap_dev) = (
         _ptr(out[n]) for n in ("lse", "colsum", "colsq", "lastp", "out_last", "recovery", "cost",
                                "cosine", "choice", "kept_pos", "kept_count", "lrr", "gap"))
+    a.topk_thr_key_dev, a.topk_thr_pos_dev = _ptr(out["thr_key"]), _ptr(out["thr_pos"])
     a.workspace_dev, a.workspace_bytes = _ptr(ws), ws_bytes
     stream = _stream()
     check(lib.akv_profile(C.byref(a), stream), ProfilerError)
@@ -340,6 +343,7 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
     c.kept_pos_dev, c.kept_count_dev, c.colsum_dev = (_ptr(out["kept_pos"]),
                                                       _ptr(out["kept_count"]), _ptr(out["colsum"]))
     c.choice_dev, c.choice_stride = _ptr(out["choice"]), nT
+    c.topk_thr_key_dev, c.topk_thr_pos_dev = _ptr(out["thr_key"]), _ptr(out["thr_pos"])
     c.n_family = F
     for i, pol in enumerate(family):
         c.family_atoms[i], c.family_r_l[i], c.family_r_f[i] = pol.bits, pol.r_l, pol.r_f
