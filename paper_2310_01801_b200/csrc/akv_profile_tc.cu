@@ -13,8 +13,10 @@
 //   colsum_j = sum_i exp(s_ij - lse_i) (engine.py:196), its square sum
 //   (profiler.py:148-161 cosine), the prompt's last row A[N-1, :] and the
 //   last-row output partial A[N-1, tile] @ V[tile] (engine.py:248,255).
-// Warp roles per CTA (192 threads): warp 0 TMA producer, warp 1 TMEM owner
-// and single-thread MMA issuer, warps 2-5 epilogue.  The fixed operand (Q
+// Warp roles per CTA (320 threads): warp 0 TMA producer, warp 1 TMEM owner
+// and single-thread MMA issuer, warps 2-9 epilogue in two column halves
+// (warps 2-5 take accumulator columns 0-63, warps 6-9 columns 64-127; the
+// halves merge their per-row / per-key results at the end).  The fixed operand (Q
 // tile in pass 1, K tile in pass 2) is loaded once; the streamed operand
 // goes through a 2-stage ring.  Grid blocks are ordered heaviest first.
 
@@ -30,7 +32,8 @@ constexpr int kTT = 128;                   // tile edge (queries / keys)
 constexpr int kBoxB = 128 * 128;           // one 128-row x 64-col bf16 box (16 KB)
 constexpr int kTileB = 2 * kBoxB;          // 128 x 128 bf16 tile (32 KB)
 constexpr int kRing = 2;                   // streamed-operand stages
-constexpr int kTcThreads = 192;            // warp0 TMA, warp1 MMA/TMEM, warps 2-5 epilogue
+constexpr int kTcThreads = 320;            // warp0 TMA, warp1 MMA/TMEM, warps 2-9 epilogue
+constexpr int kEpiWarps = 8;
 constexpr uint32_t kTmemCols = 256;        // two 128-column fp32 accumulators
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
@@ -52,7 +55,7 @@ struct TcParams {
   float scale;
 };
 
-using EpiSync = NamedSync<128, 1, 64>;
+using EpiSync = NamedSync<256, 1, 64>;
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
@@ -89,7 +92,7 @@ __global__ void __launch_bounds__(kTcThreads, 2)
   if (threadIdx.x == 0) {
     mbar_init(&q_full, 1);
     for (int s = 0; s < kRing; ++s) { mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&acc_full[a], 1); mbar_init(&acc_empty[a], 4); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&acc_full[a], 1); mbar_init(&acc_empty[a], kEpiWarps); }
     mbar_fence_init();
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
@@ -129,10 +132,13 @@ __global__ void __launch_bounds__(kTcThreads, 2)
         umma_commit(&acc_full[a]);
       }
     }
-  } else {  // ---------------- epilogue (warps 2-5) ----------------
+  } else {  // ---------------- epilogue (warps 2-9) ----------------
+    __shared__ float s_ml[kTT][2];
     const int quarter = warp & 3;
     const int et = threadIdx.x - 64;
-    const int row = qt * kTT + quarter * 32 + lane;
+    const int half = et >> 7;  // accumulator columns [64*half, 64*half + 64)
+    const int rl = quarter * 32 + lane;
+    const int row = qt * kTT + rl;
     const float sl2 = p.scale * kLog2e;
     const float slope_l2 = (p.slope ? p.slope[h] : 0.f) * kLog2e;
     const float sink_l2 = (p.sink ? p.sink[h] : 0.f) * kLog2e;
@@ -141,40 +147,43 @@ __global__ void __launch_bounds__(kTcThreads, 2)
     const float rowterm = -slope_l2 * (float)row;
     float m = -INFINITY, l = 0.f;
     uint8_t cnext = 0;
-    if (bias) cnext = et < p.N ? cls[et] : 0;
+    if (bias && et < kTT) cnext = et < p.N ? cls[et] : 0;
     for (int kt = 0; kt < nk; ++kt) {
       const int a = kt & 1;
       if (bias) {  // per-column bias of this key tile: sink on special keys + slope * col
-        const int col = kt * kTT + et;
-        s_col[a][et] = (cnext == AKV_CLS_SPECIAL ? sink_l2 : 0.f) + slope_l2 * (float)col;
-        const int nc = col + kTT;
-        cnext = (kt + 1 < nk && nc < p.N) ? cls[nc] : 0;
+        if (et < kTT) {
+          const int col = kt * kTT + et;
+          s_col[a][et] = (cnext == AKV_CLS_SPECIAL ? sink_l2 : 0.f) + slope_l2 * (float)col;
+          const int nc = col + kTT;
+          cnext = (kt + 1 < nk && nc < p.N) ? cls[nc] : 0;
+        }
         EpiSync::sync();
       }
       mbar_wait(&acc_full[a], (kt >> 1) & 1);
       tc_fence_after();
-      const bool diag = (kt == qt);
-      const bool tail = (kt + 1) * kTT > p.N;
+      const bool masked = (kt == qt) || ((kt + 1) * kTT > p.N);
 #pragma unroll 1
-      for (int ch = 0; ch < 4; ++ch) {
+      for (int ch = 2 * half; ch < 2 * half + 2; ++ch) {
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + a * kTT + ch * 32, v);
-        float cm = -INFINITY;
+        float cm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
-          const int col = kt * kTT + ch * 32 + c;
           float x = v[c] * sl2;
           if (bias) x += s_col[a][ch * 32 + c] + rowterm;
-          if ((diag && col > row) || (tail && col >= p.N)) x = -INFINITY;
+          if (masked) {
+            const int col = kt * kTT + ch * 32 + c;
+            if (col > row || col >= p.N) x = -INFINITY;
+          }
           v[c] = x;
-          cm = fmaxf(cm, x);
+          cm[c & 3] = fmaxf(cm[c & 3], x);
         }
-        const float mn = fmaxf(m, cm);
+        const float mn = fmaxf(m, fmaxf(fmaxf(cm[0], cm[1]), fmaxf(cm[2], cm[3])));
         if (mn != -INFINITY) {
-          float sum = 0.f;
+          float sm[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-          for (int c = 0; c < 32; ++c) sum += fast_exp2(v[c] - mn);
-          l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + sum;
+          for (int c = 0; c < 32; ++c) sm[c & 3] += fast_exp2(v[c] - mn);
+          l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + ((sm[0] + sm[1]) + (sm[2] + sm[3]));
           m = mn;
         }
       }
@@ -182,7 +191,16 @@ __global__ void __launch_bounds__(kTcThreads, 2)
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[a]);
     }
-    if (row < p.N) p.lse[(size_t)g * p.N + row] = (m + __log2f(l)) * kLn2;
+    // merge the two column halves of every row
+    if (half == 1) { s_ml[rl][0] = m; s_ml[rl][1] = l; }
+    EpiSync::sync();
+    if (half == 0) {
+      const float m2 = s_ml[rl][0], l2 = s_ml[rl][1];
+      const float mm = fmaxf(m, m2);
+      const float ll = (m == -INFINITY ? 0.f : l * fast_exp2(m - mm)) +
+                       (m2 == -INFINITY ? 0.f : l2 * fast_exp2(m2 - mm));
+      if (row < p.N) p.lse[(size_t)g * p.N + row] = (mm + __log2f(ll)) * kLn2;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -212,7 +230,7 @@ __global__ void __launch_bounds__(kTcThreads, 2)
   if (threadIdx.x == 0) {
     mbar_init(&k_full, 1);
     for (int s = 0; s < kRing; ++s) { mbar_init(&q_full[s], 1); mbar_init(&q_empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&acc_full[a], 1); mbar_init(&acc_empty[a], 4); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&acc_full[a], 1); mbar_init(&acc_empty[a], kEpiWarps); }
     mbar_fence_init();
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
@@ -252,10 +270,14 @@ __global__ void __launch_bounds__(kTcThreads, 2)
         umma_commit(&acc_full[a]);
       }
     }
-  } else {  // ---------------- epilogue (warps 2-5) ----------------
+  } else {  // ---------------- epilogue (warps 2-9) ----------------
+    __shared__ double s_part[2][kTT];
+    __shared__ float s_plast[kTT];
     const int quarter = warp & 3;
     const int et = threadIdx.x - 64;
-    const int key = kt * kTT + quarter * 32 + lane;
+    const int half = et >> 7;  // query columns [64*half, 64*half + 64) of every tile
+    const int kl = quarter * 32 + lane;
+    const int key = kt * kTT + kl;
     const float sl2 = p.scale * kLog2e;
     const float slope_l2 = (p.slope ? p.slope[h] : 0.f) * kLog2e;
     const float sink_l2 = (p.sink ? p.sink[h] : 0.f) * kLog2e;
@@ -267,57 +289,75 @@ __global__ void __launch_bounds__(kTcThreads, 2)
     double dsum = 0.0, dsq = 0.0;
     float lastp = 0.f;
     const int qlast = p.N - 1;
-    int q0 = kt * kTT + et;
-    float lnext = q0 < p.N ? lse[q0] : 0.f;
+    float lnext = 0.f;
+    if (et < kTT) lnext = kt * kTT + et < p.N ? lse[kt * kTT + et] : 0.f;
     for (int i = 0; i < nq; ++i) {
       const int a = i & 1;
       const int qt = kt + i;
-      {  // per-query term of this tile: -lse_q * log2e - slope * q
+      if (et < kTT) {  // per-query term of this tile: -lse_q * log2e - slope * q
         const int q = qt * kTT + et;
         s_col[a][et] = -lnext * kLog2e - slope_l2 * (float)q;
         const int qn = q + kTT;
         lnext = (i + 1 < nq && qn < p.N) ? lse[qn] : 0.f;
-        EpiSync::sync();
       }
+      EpiSync::sync();
       mbar_wait(&acc_full[a], (i >> 1) & 1);
       tc_fence_after();
-      const bool diag = (i == 0);
-      const bool tail = (qt + 1) * kTT > p.N;
-      float tsum = 0.f, tsq = 0.f;
+      // diagonal tile (causal mask), ragged tail (q >= N) and the tile holding row N-1
+      const bool masked = (i == 0) || ((qt + 1) * kTT > p.N) || (qt == qlast / kTT);
+      float ts[4] = {0.f, 0.f, 0.f, 0.f}, tq[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 1
-      for (int ch = 0; ch < 4; ++ch) {
+      for (int ch = 2 * half; ch < 2 * half + 2; ++ch) {
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + a * kTT + ch * 32, v);
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
-          const int q = qt * kTT + ch * 32 + c;
           float pr = fast_exp2(fmaf(v[c], sl2, kterm + s_col[a][ch * 32 + c]));
-          if ((diag && q < key) || (tail && q >= p.N)) pr = 0.f;
-          tsum += pr;
-          tsq = fmaf(pr, pr, tsq);
-          if (q == qlast) lastp = pr;
+          if (masked) {
+            const int q = qt * kTT + ch * 32 + c;
+            if (q < key || q >= p.N) pr = 0.f;
+            if (q == qlast) lastp = pr;
+          }
+          ts[c & 3] += pr;
+          tq[c & 3] = fmaf(pr, pr, tq[c & 3]);
         }
       }
-      dsum += (double)tsum;
-      dsq += (double)tsq;
+      dsum += (double)((ts[0] + ts[1]) + (ts[2] + ts[3]));
+      dsq += (double)((tq[0] + tq[1]) + (tq[2] + tq[3]));
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[a]);
     }
-    if (key >= p.N) lastp = 0.f;
-    if (key < p.N) {
-      p.colsum[(size_t)g * p.N + key] = dsum;
-      p.colsq[(size_t)g * p.N + key] = dsq;
-      p.lastp[(size_t)g * p.N + key] = lastp;
-    }
-    s_lastp[quarter * 32 + lane] = lastp;
+    // the last query row lies in the last (masked) tile; merge the halves
+    if (half == 1) { s_part[0][kl] = dsum; s_part[1][kl] = dsq; s_plast[kl] = lastp; }
     EpiSync::sync();
-    // last-row output partial of this key tile: sum_j lastp_j V_j (d = 128 = one dim per thread)
-    const __nv_bfloat16* vt = p.v + ((size_t)g * p.ld + (size_t)kt * kTT) * 128;
-    const int nrow = min(kTT, p.N - kt * kTT);
-    float o = 0.f;
-    for (int j = 0; j < nrow; ++j) o = fmaf(s_lastp[j], __bfloat162float(vt[(size_t)j * 128 + et]), o);
-    p.out_part[((size_t)g * ntiles + kt) * 128 + et] = o;
+    if (half == 0) {
+      dsum += s_part[0][kl];
+      dsq += s_part[1][kl];
+      lastp += s_plast[kl];
+      if (key >= p.N) lastp = 0.f;
+      if (key < p.N) {
+        p.colsum[(size_t)g * p.N + key] = dsum;
+        p.colsq[(size_t)g * p.N + key] = dsq;
+        p.lastp[(size_t)g * p.N + key] = lastp;
+      }
+      s_lastp[kl] = lastp;
+    }
+    EpiSync::sync();
+    if (half == 0) {
+      // last-row output partial of this key tile: sum_j lastp_j V_j (d = 128 = one dim per thread)
+      const __nv_bfloat16* vt = p.v + ((size_t)g * p.ld + (size_t)kt * kTT) * 128;
+      const int nrow = min(kTT, p.N - kt * kTT);
+      float o[4] = {0.f, 0.f, 0.f, 0.f};
+      int j = 0;
+      for (; j + 4 <= nrow; j += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          o[u] = fmaf(s_lastp[j + u], __bfloat162float(vt[(size_t)(j + u) * 128 + et]), o[u]);
+      }
+      for (; j < nrow; ++j) o[0] = fmaf(s_lastp[j], __bfloat162float(vt[(size_t)j * 128 + et]), o[0]);
+      p.out_part[((size_t)g * ntiles + kt) * 128 + et] = (o[0] + o[1]) + (o[2] + o[3]);
+    }
   }
   tc_fence_before();
   __syncthreads();
