@@ -193,6 +193,58 @@ int akv_decode_step(const akv_decode_args* a, void* stream);
 int akv_decode_workspace_init(void* workspace_dev, size_t workspace_bytes, int32_t B, int32_t H,
                               int32_t d, int32_t max_cap, int64_t total_slots, void* stream);
 
+
+/* ---- reference single-context operations (float64, batched) ----------
+ * The reference's building blocks besides the fused session path, so the
+ * Python mirror of attention.py / policies.py / profiler.py runs on the GPU.
+ */
+/* attention.py:64-89 softmax_rows: row r normalised over its first lengths[r]
+ * columns (all columns when lengths is NULL), the rest exactly 0 */
+int akv_softmax_rows_f64(int32_t rows, int32_t cols, const double* in_dev,
+                         const int32_t* lengths_dev, double* out_dev, void* stream);
+/* attention.py:102-127 causal_attention: A = causal softmax(q k^T * scale), O = A v */
+int akv_causal_attention_f64(int32_t n, int32_t dq, int32_t dv, const double* q_dev,
+                             const double* k_dev, const double* v_dev, double scale,
+                             double* A_dev, double* O_dev, void* stream);
+
+/* policies.py:214-267 retained_indices over G independent contexts (one
+ * policy each); count = cache_memory_cost (policies.py:291-293) */
+typedef struct akv_keep_args {
+  int32_t G;
+  int32_t stride;                 /* positions per context row (>= every current_len) */
+  const int32_t* prompt_len_dev;  /* [G] */
+  const int32_t* current_len_dev; /* [G] */
+  const uint8_t* cls_dev;         /* [G,stride] class per position */
+  const double* score_dev;        /* [G,stride] cumulative scores */
+  const uint8_t* cand_dev;        /* [G,stride] candidate flags, or NULL (all < current_len) */
+  const uint8_t* atoms_dev;       /* [G] policy atoms */
+  const double* r_l_dev;          /* [G] */
+  const double* r_f_dev;          /* [G] */
+  uint8_t* keep_dev;              /* [G,stride] out */
+  int32_t* count_dev;             /* [G] out */
+  int32_t* scratch_dev;           /* [G,stride] workspace */
+} akv_keep_args;
+int akv_keep_mask(const akv_keep_args* a, void* stream);
+
+/* profiler.py:70-87 recovery_ratio and :148-161 masked_cosine_similarity of
+ * F retained masks on each of G dense maps A [G,n,n] */
+int akv_map_recovery_f64(int32_t G, int32_t n, const double* A_dev, int32_t F,
+                         const uint8_t* masks_dev, int32_t rows, double* colsum_ws_dev,
+                         double* colsq_ws_dev, double* recovery_dev, double* cosine_dev,
+                         void* stream);
+/* policies.py:332-360 update_cumulative_scores: out[:L] = in, out[L] = 0,
+ * out[retained[t]] += row[t] */
+int akv_update_scores_f64(int32_t L, const double* scores_in_dev, int32_t m,
+                          const int32_t* retained_dev, const double* row_dev,
+                          double* scores_out_dev, void* stream);
+/* policies.py:270-288 apply_policy: Kc[r] = K[idx[r]], Vc[r] = V[idx[r]] */
+int akv_gather_rows_f64(int32_t dk, int32_t dv, const double* K_dev, const double* V_dev,
+                        int32_t m, const int32_t* idx_dev, double* Kc_dev, double* Vc_dev,
+                        void* stream);
+/* profiler.py:51-67 tv_distance_row */
+int akv_tv_distance_f64(int32_t n, const double* p_dev, const uint8_t* mask_dev, double* out_dev,
+                        void* stream);
+
 /* ---- misc ------------------------------------------------------------ */
 const char* akv_last_error(void);
 const char* akv_version(void);

@@ -8,15 +8,20 @@ calls fail unless an sm_100 device is present.  There is no CPU fallback.
 """
 
 from ._lib import AkvError, lib as _lib_handle  # noqa: F401  (loads the .so)
+from .attention import (AttentionError, AttentionMap, causal_attention, softmax_rows,
+                        softmax_vector)
 from .engine import (CompressedCache, EngineError, GenerationConfig, GenerationResult,
                      GreedyArgmax, Nucleus, ProfileResult, StepRecord, decode_step_tensors,
                      encode_prompt, encode_prompt_tensors, generate, generate_fixed_baseline,
                      generate_step, records_to_ndjson, reference_generate)
 from .policies import (DEFAULT_FEASIBLE_ORDER, DEFAULT_RATIO, CompressionPolicy, PolicyAtom,
-                       PolicyError, RetainedSet, feasible_set, format_policy, full_policy,
-                       parse_policy)
+                       PolicyContext, PolicyError, RetainedSet, apply_policy, cache_memory_cost,
+                       feasible_set, format_policy, full_policy, local_budget, parse_policy,
+                       retained_indices, update_cumulative_scores)
 from .profiler import (HeadDecision, HeadProfile, ProfilerConfig, ProfilerError, RecoveryReport,
-                       RowAveraging, SelectionCriterion)
+                       RowAveraging, SelectionCriterion, evaluate_policy, masked_cosine_similarity,
+                       profile_model, recovery_ratio, select_policy, select_policy_by_similarity,
+                       tv_distance_row)
 from .tokens import TokenAnnotation, TokenClass, VocabMetadata, classify_tokens
 
 __version__ = "0.1.0"

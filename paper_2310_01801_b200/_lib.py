@@ -67,10 +67,20 @@ class DecodeArgs(C.Structure):
     ]
 
 
+class KeepArgs(C.Structure):
+    _fields_ = [
+        ("G", i32), ("stride", i32), ("prompt_len_dev", P), ("current_len_dev", P),
+        ("cls_dev", P), ("score_dev", P), ("cand_dev", P), ("atoms_dev", P), ("r_l_dev", P),
+        ("r_f_dev", P), ("keep_dev", P), ("count_dev", P), ("scratch_dev", P),
+    ]
+
+
 # every symbol include/akv.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "akv_profile_workspace_size", "akv_profile", "akv_compact", "akv_plan_segments",
     "akv_decode_workspace_size", "akv_decode_step", "akv_decode_workspace_init",
+    "akv_softmax_rows_f64", "akv_causal_attention_f64", "akv_keep_mask", "akv_map_recovery_f64",
+    "akv_update_scores_f64", "akv_gather_rows_f64", "akv_tv_distance_f64",
     "akv_last_error", "akv_version", "akv_device_check",
 )
 
@@ -95,6 +105,17 @@ def _load():
     lib.akv_decode_step.argtypes = [C.POINTER(DecodeArgs), P]
     lib.akv_decode_workspace_init.restype = C.c_int
     lib.akv_decode_workspace_init.argtypes = [P, sz, i32, i32, i32, i32, i64, P]
+    lib.akv_softmax_rows_f64.argtypes = [i32, i32, P, P, P, P]
+    lib.akv_causal_attention_f64.argtypes = [i32, i32, i32, P, P, P, f64, P, P, P]
+    lib.akv_keep_mask.argtypes = [C.POINTER(KeepArgs), P]
+    lib.akv_map_recovery_f64.argtypes = [i32, i32, P, i32, P, i32, P, P, P, P, P]
+    lib.akv_update_scores_f64.argtypes = [i32, P, i32, P, P, P, P]
+    lib.akv_gather_rows_f64.argtypes = [i32, i32, P, P, i32, P, P, P, P]
+    lib.akv_tv_distance_f64.argtypes = [i32, P, P, P, P]
+    for fn in ("akv_softmax_rows_f64", "akv_causal_attention_f64", "akv_keep_mask",
+               "akv_map_recovery_f64", "akv_update_scores_f64", "akv_gather_rows_f64",
+               "akv_tv_distance_f64"):
+        getattr(lib, fn).restype = C.c_int
     lib.akv_last_error.restype = C.c_char_p
     lib.akv_version.restype = C.c_char_p
     lib.akv_device_check.restype = C.c_int
