@@ -176,6 +176,10 @@ typedef struct akv_decode_args {
   void* vc_dev;
   int32_t* meta_dev;
   double* score_dev;
+  const int32_t* base_live_dev;  /* [B*H] live slots right after compaction (akv_compact's live):
+                                    base_live + (pos - prompt_len) bounds live_in and equals it
+                                    for full-cache heads, which lets a step start streaming
+                                    before the previous step has drained */
   const int32_t* live_in_dev;    /* [B*H] live slots before the step */
   int32_t* live_out_dev;         /* [B*H] live slots after insert+evict (distinct buffer) */
   float* out_dev;                /* [B,H,d] attention output (fp32) */

@@ -61,7 +61,7 @@ class DecodeArgs(C.Structure):
         ("q_dev", P), ("k_dev", P), ("v_dev", P), ("bh_stride", i64), ("new_cls_dev", P),
         ("slope_dev", P), ("sink_dev", P), ("head_atoms_dev", P), ("head_r_l_dev", P),
         ("head_r_f_dev", P), ("seg_off_dev", P), ("seg_cap_dev", P), ("kc_dev", P),
-        ("vc_dev", P), ("meta_dev", P), ("score_dev", P), ("live_in_dev", P),
+        ("vc_dev", P), ("meta_dev", P), ("score_dev", P), ("base_live_dev", P), ("live_in_dev", P),
         ("live_out_dev", P), ("out_dev", P), ("evicted_dev", P), ("status_dev", P),
         ("max_cap", i32), ("total_slots", i64), ("workspace_dev", P), ("workspace_bytes", sz),
     ]

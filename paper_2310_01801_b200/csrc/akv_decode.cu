@@ -75,6 +75,7 @@ struct DecParams {
   void* vc;
   int32_t* meta;
   double* score;
+  const int32_t* base_live;
   const int32_t* live_in;
   int32_t* live_out;
   float* out;
@@ -164,6 +165,46 @@ __device__ __forceinline__ long long plan_pages(const DecParams& p, int page, in
   if (threadIdx.x == 0) s_prefix[G] = total;
   __syncthreads();
   return s_prefix[G];
+}
+
+// Page plan from live-count BOUNDS (base_live + step), computable before
+// the previous step has finished: exact for full-cache heads (their live
+// count grows by one per step), an upper bound otherwise (surplus pages are
+// streamed as empty).  s_full marks full-cache heads.
+__device__ __forceinline__ long long plan_pages_bound(const DecParams& p, int page, int step,
+                                                      int* s_prefix, int* s_live,
+                                                      uint8_t* s_full, int* red_i) {
+  const int G = p.G;
+  const int per = (G + blockDim.x - 1) / blockDim.x;
+  const int lo = min(G, (int)threadIdx.x * per), hi = min(G, lo + per);
+  int cnt = 0;
+  for (int g = lo; g < hi; ++g) {
+    const int bound = min(p.base_live[g] + step, p.seg_cap[g] - 1);
+    s_live[g] = bound;
+    s_full[g] = (p.atoms[g] & AKV_ATOM_FULL) ? 1 : 0;
+    cnt += (bound + 1 + page - 1) / page;
+  }
+  int total;
+  int off = block_exclusive_scan<BlockSync>(cnt, red_i, &total);
+  for (int g = lo; g < hi; ++g) {
+    s_prefix[g] = off;
+    off += (s_live[g] + 1 + page - 1) / page;
+  }
+  if (threadIdx.x == 0) s_prefix[G] = total;
+  __syncthreads();
+  return s_prefix[G];
+}
+
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// live count of a non-full head, read after the previous step completed
+__device__ __forceinline__ int live_after_wait(const DecParams& p, int g) {
+  int L = p.live_in[g];
+  if (L + 1 > p.seg_cap[g]) {  // capacity overflow: flag it, keep writes in bounds
+    atomicExch(p.status, AKV_ERR_CAPACITY);
+    L = p.seg_cap[g] - 1;
+  }
+  return L;
 }
 
 // largest g with s_prefix[g] <= pg
@@ -886,6 +927,7 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
   const int G = p.G;
   int* s_prefix = reinterpret_cast<int*>(smem + kStages * S::STAGE_B);
   int* s_live = s_prefix + (G + 1);
+  uint8_t* s_full = reinterpret_cast<uint8_t*>(s_live + G);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   AKV_TRACE(0);
   if (tid == 0) {
@@ -895,11 +937,17 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
   }
-  // PDL: everything above overlaps the previous step's tail; live_in and the
-  // arena are read only after the previous grid has completed
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  const long long P = plan_pages(p, PAGE, s_prefix, s_live, red_i);
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // Programmatic dependent launch.  When the previous launch on the stream
+  // is the previous decode step (step > 0), its CTAs signalled only after
+  // their own predecessor had completed, so every arena row below slot
+  // live-1 of a full-cache head is already final: those pages stream
+  // before griddepcontrol.wait.  Anything the previous step writes (its
+  // inserted row, live counts and rows of evicting heads, semaphores,
+  // partials, outputs) is touched only after the wait.
+  const int step = p.pos - p.prompt_len;
+  const bool early = step > 0;
+  if (!early) grid_dep_wait();
+  const long long P = plan_pages_bound(p, PAGE, step, s_prefix, s_live, s_full, red_i);
   AKV_TRACE(1);
   const int grid = (int)(P < (long long)gridDim.x ? P : (long long)gridDim.x);
   if ((int)blockIdx.x >= grid) return;
@@ -910,14 +958,25 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
   if (warp == NW) {  // ---------------- producer ----------------
     if (lane == 0) {
       const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
-      int g = g0, stage = 0;
+      bool waited = !early;
+      int g = g0, stage = 0, gl = -1, L = 0;
       uint32_t phase = 0;
       for (long long pg = pbeg; pg < pend; ++pg) {
         while (pg >= s_prefix[g + 1]) ++g;
-        const int L = s_live[g];
+        if (g != gl) {
+          gl = g;
+          if (s_full[g]) {
+            L = s_live[g];
+          } else {
+            if (!waited) { grid_dep_wait(); waited = true; }
+            L = live_after_wait(p, g);
+          }
+        }
         const int slot0 = (int)(pg - s_prefix[g]) * PAGE;
         const int rows = max(0, min(PAGE, L - slot0));
         const bool has_new = (L >= slot0 && L < slot0 + PAGE);
+        // the previous step wrote row L-1 of a full head; a page holding it waits
+        if (!waited && slot0 + rows > L - 1) { grid_dep_wait(); waited = true; }
         mbar_wait(&empty_bar[stage], phase ^ 1);
         uint8_t* st = smem + stage * S::STAGE_B;
         const int64_t base = p.seg_off[g];
@@ -950,6 +1009,10 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
   }
 
   if (warp > NW) {  // ---------------- epilogue warps ----------------
+    // semaphores, partials, outputs and policy state belong to the previous
+    // step until it completes; once it has, dependents may launch
+    grid_dep_wait();
+    if (warp == NW + 1 && lane == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     // one published segment per head touched by this CTA's page range, in order
     int pub_n = 0;
     for (int g = g0; g < G && s_prefix[g] < pend; ++g) {
@@ -983,7 +1046,14 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
 
   for (long long pg = pbeg; pg < pend; ++pg) {
     while (pg >= s_prefix[g + 1]) ++g;
-    if (g != hc.g) load_head(p, g, s_live[g], hc);
+    if (g != hc.g) {
+      int Lh = s_live[g];
+      if (!s_full[g]) {  // evicting head: its live count comes from the previous step
+        if (early) grid_dep_wait();
+        Lh = live_after_wait(p, g);
+      }
+      load_head(p, g, Lh, hc);
+    }
     const int L = hc.L, n = hc.n;
     const int slot0 = (int)(pg - s_prefix[g]) * PAGE;
     mbar_wait(&full_bar[stage], phase);
@@ -1200,13 +1270,13 @@ static cudaError_t launch_mma(const DecParams& p, int64_t total_slots, cudaStrea
   cudaError_t e;
   if (!attr) {
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(1024 + kStages * S::STAGE_B + (2 * kMaxHeads + 1) * 4))))
+                                  (int)(1024 + kStages * S::STAGE_B + (2 * kMaxHeads + 1) * 4 + kMaxHeads))))
       return e;
     attr = true;
   }
   int sms;
   if ((e = num_sms(&sms))) return e;
-  const size_t smem = 1024 + (size_t)kStages * S::STAGE_B + (size_t)(2 * p.G + 1) * 4;
+  const size_t smem = 1024 + (size_t)kStages * S::STAGE_B + (size_t)(2 * p.G + 1) * 4 + p.G;
   return launch_pdl(kern, 2 * sms, S::THREADS, smem, st, p, g_tmaps.k, g_tmaps.v);
 }
 
@@ -1282,7 +1352,8 @@ extern "C" int akv_decode_step(const akv_decode_args* a, void* stream) {
   DecParams p{a->B, a->H, a->B * a->H, a->prompt_len, a->pos, a->q_dev, a->k_dev, a->v_dev,
               a->bh_stride, a->new_cls_dev, a->slope_dev, a->sink_dev, a->head_atoms_dev,
               a->head_r_l_dev, a->head_r_f_dev, a->seg_off_dev, a->seg_cap_dev, a->kc_dev, a->vc_dev,
-              a->meta_dev, a->score_dev, a->live_in_dev, a->live_out_dev, a->out_dev,
+              a->meta_dev, a->score_dev, a->base_live_dev, a->live_in_dev, a->live_out_dev,
+              a->out_dev,
               a->evicted_dev, a->status_dev ? a->status_dev : w.status, w.part, w.logit, w.counter,
               w.max_parts, (float)(1.0 / sqrt((double)a->d)), g_dec_trace};
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -328,6 +328,7 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
     cache.meta = torch.empty(cache.total_slots, dtype=i32, device=dev)
     cache.score = torch.empty(cache.total_slots, dtype=f64, device=dev)
     cache.live_buf = [torch.empty(G, dtype=i32, device=dev), torch.empty(G, dtype=i32, device=dev)]
+    cache.base_live = torch.empty(G, dtype=i32, device=dev)
     cache.out = out["out_last"]
     cache.evicted = torch.zeros(G, dtype=i32, device=dev)
     cache.status = torch.zeros(1, dtype=i32, device=dev)
@@ -354,6 +355,7 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
                                                    _ptr(cache.meta), _ptr(cache.score))
     c.live_dev = _ptr(cache.live_buf[0])
     check(lib.akv_compact(C.byref(c), stream), EngineError)
+    cache.base_live.copy_(cache.live_buf[0])  # the decode's live-count bound anchor
 
     ws_bytes = lib.akv_decode_workspace_size(B, H, d, cache.max_cap, cache.total_slots)
     cache.workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
@@ -372,6 +374,7 @@ def _decode_args(cache: CompressedCache, dt: int) -> DecodeArgs:
     a.seg_off_dev, a.seg_cap_dev = _ptr(cache.seg_off), _ptr(cache.seg_cap)
     a.kc_dev, a.vc_dev, a.meta_dev, a.score_dev = (_ptr(cache.kc), _ptr(cache.vc),
                                                    _ptr(cache.meta), _ptr(cache.score))
+    a.base_live_dev = _ptr(cache.base_live)
     a.out_dev, a.evicted_dev, a.status_dev = _ptr(cache.out), _ptr(cache.evicted), _ptr(cache.status)
     a.max_cap, a.total_slots = cache.max_cap, cache.total_slots
     a.workspace_dev, a.workspace_bytes = _ptr(cache.workspace), cache.workspace.numel()
