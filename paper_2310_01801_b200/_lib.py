@@ -145,6 +145,17 @@ def check(rc: int, exc_invalid=None):
     raise AkvError(rc, msg)
 
 
+_checked_devices = set()
+
+
 def require_device():
-    """Fail loudly unless a sm_100 device is current (no CPU fallback)."""
-    check(lib.akv_device_check())
+    """Fail loudly unless a sm_100 device is current (no CPU fallback).
+    Checked once per device per process."""
+    import torch
+
+    if not torch.cuda.is_available():
+        check(lib.akv_device_check())
+    dev = torch.cuda.current_device()
+    if dev not in _checked_devices:
+        check(lib.akv_device_check())
+        _checked_devices.add(dev)

@@ -34,12 +34,13 @@ extern "C" int akv_device_check(void) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return set_error(AKV_ERR_CUDA, "no CUDA device: %s", cudaGetErrorString(e));
-  cudaDeviceProp prop;
-  e = cudaGetDeviceProperties(&prop, dev);
-  if (e != cudaSuccess) return set_error(AKV_ERR_CUDA, "%s", cudaGetErrorString(e));
-  if (prop.major != 10 || prop.minor != 0)
-    return set_error(AKV_ERR_UNSUPPORTED, "device %s is sm_%d%d; this library is built for sm_100a",
-                     prop.name, prop.major, prop.minor);
+  int major = 0, minor = 0;
+  if ((e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev)) != cudaSuccess ||
+      (e = cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev)) != cudaSuccess)
+    return set_error(AKV_ERR_CUDA, "%s", cudaGetErrorString(e));
+  if (major != 10 || minor != 0)
+    return set_error(AKV_ERR_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a",
+                     dev, major, minor);
   return AKV_OK;
 }
 
