@@ -249,6 +249,47 @@ int akv_gather_rows_f64(int32_t dk, int32_t dv, const double* K_dev, const doubl
 int akv_tv_distance_f64(int32_t n, const double* p_dev, const uint8_t* mask_dev, double* out_dev,
                         void* stream);
 
+/* ---- model caller (multi-layer decoder around K1-K3) ------------------
+ * The per-layer glue of a Llama-style decoder that produces the q/k/v rows
+ * the reference's model protocol hands to the engine (model.py:219-286)
+ * and consumes the concatenated head outputs (engine.py:354-357).  dtype is
+ * AKV_DTYPE_F32 or AKV_DTYPE_BF16 for every tensor of a call; rows are
+ * contiguous and 16-byte aligned. */
+/* x_out[t] = emb[ids[t]] (emb may be NULL), cls_out[t] = lut[ids[t]] (may be NULL) */
+int akv_embed_classify(int32_t n, const int64_t* ids_dev, int32_t vocab, const uint8_t* lut_dev,
+                       const void* emb_dev, int32_t dm, int32_t dtype, void* x_out_dev,
+                       uint8_t* cls_out_dev, void* stream);
+/* residual += x (x may be NULL); out = residual * rsqrt(mean(residual^2) + eps) * w */
+int akv_add_rmsnorm(int32_t rows, int32_t dim, int32_t dtype, const void* x_dev,
+                    void* residual_dev, const void* w_dev, float eps, void* out_dev,
+                    void* stream);
+typedef struct akv_rope_args {
+  int32_t T;                  /* token rows of qkv; T % n == 0 */
+  int32_t n;                  /* rows per sequence: token t = b*n + i */
+  int32_t Hl, d, dtype;       /* heads in this projection, head dim */
+  const void* qkv_dev;        /* row t: [q heads Hl*d | k heads Hl*d | v heads Hl*d] */
+  int64_t qkv_ld;             /* elements between rows of qkv */
+  int32_t pos0;               /* RoPE position of i = 0 */
+  int32_t max_pos;            /* rows of the cos/sin tables */
+  const float* cos_dev;       /* [max_pos, d/2] */
+  const float* sin_dev;
+  void* q_dev;                /* out [B, Hl, out_ld, d]: token (b, i) -> row row0 + i */
+  void* k_dev;
+  void* v_dev;
+  int64_t out_ld;
+  int32_t row0;
+} akv_rope_args;
+/* rotate-half RoPE of q and k, copy of v, scattered head-major */
+int akv_rope_scatter(const akv_rope_args* a, void* stream);
+/* out[r, c] = silu(gu[r, c]) * gu[r, F + c] */
+int akv_swiglu(int32_t rows, int32_t F, int32_t dtype, const void* gu_dev, void* out_dev,
+               void* stream);
+/* tokens[b] = first argmax of logits[b, :V]; cls[b] = lut[token] (may be NULL);
+ * x_out[b] = emb[token] (emb may be NULL) */
+int akv_greedy_next(int32_t B, int32_t V, int32_t dtype, const void* logits_dev, int64_t ld,
+                    const uint8_t* lut_dev, const void* emb_dev, int32_t dm, int64_t* tokens_dev,
+                    uint8_t* cls_dev, void* x_out_dev, void* stream);
+
 /* ---- misc ------------------------------------------------------------ */
 const char* akv_last_error(void);
 const char* akv_version(void);

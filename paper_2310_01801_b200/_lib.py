@@ -75,13 +75,22 @@ class KeepArgs(C.Structure):
     ]
 
 
+class RopeArgs(C.Structure):
+    _fields_ = [
+        ("T", i32), ("n", i32), ("Hl", i32), ("d", i32), ("dtype", i32), ("qkv_dev", P),
+        ("qkv_ld", i64), ("pos0", i32), ("max_pos", i32), ("cos_dev", P), ("sin_dev", P),
+        ("q_dev", P), ("k_dev", P), ("v_dev", P), ("out_ld", i64), ("row0", i32),
+    ]
+
+
 # every symbol include/akv.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "akv_profile_workspace_size", "akv_profile", "akv_compact", "akv_plan_segments",
     "akv_decode_workspace_size", "akv_decode_step", "akv_decode_workspace_init",
     "akv_softmax_rows_f64", "akv_causal_attention_f64", "akv_keep_mask", "akv_map_recovery_f64",
     "akv_update_scores_f64", "akv_gather_rows_f64", "akv_tv_distance_f64",
-    "akv_last_error", "akv_version", "akv_device_check",
+    "akv_embed_classify", "akv_add_rmsnorm", "akv_rope_scatter", "akv_swiglu",
+    "akv_greedy_next", "akv_last_error", "akv_version", "akv_device_check",
 )
 
 
@@ -112,7 +121,13 @@ def _load():
     lib.akv_update_scores_f64.argtypes = [i32, P, i32, P, P, P, P]
     lib.akv_gather_rows_f64.argtypes = [i32, i32, P, P, i32, P, P, P, P]
     lib.akv_tv_distance_f64.argtypes = [i32, P, P, P, P]
-    for fn in ("akv_softmax_rows_f64", "akv_causal_attention_f64", "akv_keep_mask",
+    lib.akv_embed_classify.argtypes = [i32, P, i32, P, P, i32, i32, P, P, P]
+    lib.akv_add_rmsnorm.argtypes = [i32, i32, i32, P, P, P, C.c_float, P, P]
+    lib.akv_rope_scatter.argtypes = [C.POINTER(RopeArgs), P]
+    lib.akv_swiglu.argtypes = [i32, i32, i32, P, P, P]
+    lib.akv_greedy_next.argtypes = [i32, i32, i32, P, i64, P, P, i32, P, P, P, P]
+    for fn in ("akv_embed_classify", "akv_add_rmsnorm", "akv_rope_scatter", "akv_swiglu",
+               "akv_greedy_next", "akv_softmax_rows_f64", "akv_causal_attention_f64", "akv_keep_mask",
                "akv_map_recovery_f64", "akv_update_scores_f64", "akv_gather_rows_f64",
                "akv_tv_distance_f64"):
         getattr(lib, fn).restype = C.c_int

@@ -9,10 +9,13 @@ cross-head reads), so the path partitions with no data-path collective:
 * ``batch_shard``: contiguous batch rows per rank (independent sessions,
   what bench.py's weak-scaling run does).
 
-The only communication is host-side bookkeeping: gathering the per-rank
-profile rows (HeadProfile CSV) and, for verification, the outputs.  The
-multi-layer configs' all-gather of attention outputs is SURVEY §8(f)
-'next' and is not implemented here.
+For the single-layer configs the only communication is host-side
+bookkeeping: gathering the per-rank profile rows (HeadProfile CSV) and, for
+verification, the outputs.  The multi-layer caller (``llama.py``, configs
+2/3) adds the data-path collectives below: the all-gather of head-sharded
+attention outputs (``gather_head_blocks``) and, in tensor-parallel mode,
+the all-reduce of row-parallel partial sums (``all_reduce_partial``); the
+weight slicing both modes use is ``shard_layer_weights``.
 """
 
 from __future__ import annotations
@@ -88,3 +91,61 @@ def profile_csv(rows: list) -> str:
     lines = ["layer,head,policy,recovery,cost_tokens"]
     lines += [f"{b},{h},{p},{rec!r},{c}" for b, h, p, rec, c in rows]
     return "\n".join(lines) + "\n"
+
+
+def shard_layer_weights(mats: dict, h0: int, h1: int, d: int, f0: int, f1: int, mode: str):
+    """Local weights of one decoder layer from its full matrices
+    (``wq, wk, wv, wo`` [dm, dm], ``wg, wu`` [F, dm], ``wd`` [dm, F]):
+
+    * wqkv [3*Hl*d, dm] - rows of heads [h0, h1) of q, k and v (column
+      parallel: each rank projects only its own heads);
+    * wo - full [dm, H*d] in ``gather`` mode (outputs are all-gathered
+      first), the columns of the local heads [dm, Hl*d] in ``tp`` mode
+      (row parallel, partial sums all-reduced);
+    * wgu [2*Fl, dm] - gate rows [f0, f1) then up rows [f0, f1);
+    * wdown [dm, Fl] - columns [f0, f1).
+    """
+    hs = slice(h0 * d, h1 * d)
+    fs = slice(f0, f1)
+    wqkv = _cat([mats["wq"][hs], mats["wk"][hs], mats["wv"][hs]])
+    wo = mats["wo"] if mode != "tp" else mats["wo"][:, hs].contiguous()
+    wgu = _cat([mats["wg"][fs], mats["wu"][fs]])
+    wdown = mats["wd"][:, fs].contiguous()
+    return wqkv, wo, wgu, wdown
+
+
+def _cat(parts):
+    import torch
+
+    return torch.cat(parts).contiguous()
+
+
+def gather_head_blocks(o, world: int, group=None):
+    """All-gather head-sharded attention outputs: ``o`` [rows, Hl*d] on every
+    rank -> [rows, world*Hl*d] with rank r's block at columns
+    [r*Hl*d, (r+1)*Hl*d) - the global head order, since rank r owns the
+    contiguous heads [r*Hl, (r+1)*Hl).  NCCL uses one
+    all_gather_into_tensor; other backends (gloo, CPU tests) a list gather."""
+    if world == 1:
+        return o
+    import torch
+    import torch.distributed as dist
+
+    o = o.contiguous()
+    rows = o.shape[0]
+    if o.is_cuda:
+        buf = torch.empty(world, rows, o.shape[1], dtype=o.dtype, device=o.device)
+        dist.all_gather_into_tensor(buf, o, group=group)
+        return buf.permute(1, 0, 2).reshape(rows, -1)
+    parts = [torch.empty_like(o) for _ in range(world)]
+    dist.all_gather(parts, o, group=group)
+    return torch.cat(parts, dim=1)
+
+
+def all_reduce_partial(x, world: int, group=None):
+    """Sum row-parallel partial products over the ranks (in place)."""
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(x, group=group)
+    return x

@@ -1,0 +1,228 @@
+"""Multi-layer caller (paper_2310_01801_b200/llama.py) on the GPU.
+
+1. Full-cache policy: the model through the caller kernels + K1/K2/K3 must
+   match a plain PyTorch fp32 Llama that recomputes full causal attention
+   over the whole sequence at every step (logits within 1e-4 of max|logit|,
+   identical greedy tokens).
+2. Adaptive policies inside the model: every layer's recorded q/k/v rows
+   (prompt + every decode step) are replayed through the CPU oracle; the
+   per-head policies, the final kept sets and the per-step attention outputs
+   of every layer must match (bit-exact sets, rtol 1e-4 outputs), except
+   heads within 1e-4 of T (listed separately).
+3. The caller kernels against torch on their own (rmsnorm, rope, swiglu,
+   greedy argmax + class + embedding), fp32 and bf16.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import akv_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+SPECIAL = (1,)
+PUNCT = tuple(range(5, 21))
+
+
+def _tiny(n_layers=2):
+    from paper_2310_01801_b200.llama import LlamaConfig
+
+    return LlamaConfig(n_layers=n_layers, d_model=256, n_heads=4, ffn=512, vocab=512)
+
+
+def _prompt(B, N, vocab, seed=0):
+    rng = np.random.default_rng(seed)
+    ids = rng.integers(21, vocab, size=(B, N))
+    punct = rng.random((B, N)) < 0.1
+    ids = np.where(punct, rng.choice(PUNCT, size=(B, N)), ids)
+    ids[:, 0] = SPECIAL[0]
+    return torch.from_numpy(ids).cuda()
+
+
+def _model(cfg, dtype=torch.float32, seed=3):
+    from paper_2310_01801_b200.llama import FastGenLlama
+
+    return FastGenLlama(cfg, dtype=dtype, seed=seed, special_ids=SPECIAL, punct_ids=PUNCT,
+                        max_positions=512)
+
+
+def _torch_forward(m, ids):
+    """Plain fp32 Llama over the full sequence ids [B, T] -> logits [B, T, V]."""
+    cfg = m.cfg
+    d, H = cfg.head_dim, cfg.n_heads
+    B, T = ids.shape
+    f = lambda t: t.float()  # noqa: E731
+
+    def rms(x, w):
+        return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + cfg.eps) * f(w)
+
+    cos, sin = m.cos[:T], m.sin[:T]
+
+    def rope(x):  # [B, T, H, d]
+        x1, x2 = x[..., : d // 2], x[..., d // 2:]
+        c, s = cos[None, :, None, :], sin[None, :, None, :]
+        return torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], dim=-1)
+
+    x = f(m.embed)[ids]
+    mask = torch.ones(T, T, dtype=torch.bool, device=ids.device).tril()
+    for L in m.layers:
+        xn = rms(x, L.attn_norm)
+        qkv = xn @ f(L.wqkv).T
+        q, k, v = qkv.view(B, T, 3, H, d).unbind(2)
+        q, k = rope(q), rope(k)
+        s = torch.einsum("bihd,bjhd->bhij", q, k) / d ** 0.5
+        s = s.masked_fill(~mask, float("-inf"))
+        o = torch.einsum("bhij,bjhd->bihd", s.softmax(-1), v).reshape(B, T, H * d)
+        x = x + o @ f(L.wo).T
+        xn = rms(x, L.mlp_norm)
+        gu = xn @ f(L.wgu).T
+        g, u = gu[..., : cfg.ffn], gu[..., cfg.ffn:]
+        x = x + (torch.nn.functional.silu(g) * u) @ f(L.wdown).T
+    return rms(x, m.final_norm) @ f(m.lm_head).T
+
+
+def test_llama_full_policy_matches_torch_reference():
+    from paper_2310_01801_b200 import full_policy
+
+    torch.backends.cuda.matmul.allow_tf32 = False
+    cfg = _tiny()
+    m = _model(cfg)
+    B, N, D = 2, 48, 6
+    ids = _prompt(B, N, cfg.vocab)
+    m.prefill(ids, fixed_policy=full_policy(), max_new_tokens=D)
+    seq = ids
+    for t in range(D + 1):
+        ref = _torch_forward(m, seq)[:, -1]
+        got = m.last_logits.float()
+        scale = ref.abs().max().item()
+        assert torch.allclose(got, ref, rtol=0, atol=1e-4 * scale), (
+            t, (got - ref).abs().max().item(), scale)
+        top2 = ref.topk(2, dim=-1).values
+        nxt = m.next_tok.clone()
+        clear = (top2[:, 0] - top2[:, 1]) > 1e-3 * scale
+        assert torch.equal(nxt[clear], ref.argmax(-1)[clear])
+        if t == D:
+            break
+        ins = m.decode_step()
+        seq = torch.cat([seq, ins[:, None]], dim=1)
+    assert m.cache_tokens() == cfg.n_layers * B * cfg.n_heads * (N + D)
+    m.check()
+
+
+def _replay_layer(m, li, cfg_family, thresholds, fixed, steps):
+    """Oracle session on layer li's recorded rows; returns (session, outs)."""
+    q, k, v = (x.double().cpu().numpy() for x in m.trace["prompt"][li])
+    B, Hl, N, d = q.shape
+    cls = m.classes[:, :N].cpu().numpy().astype(np.int64)
+    zeros = np.zeros(Hl)
+    sess = O.encode_session(q, k, v, cls, zeros, zeros, cfg_family, thresholds, fixed=fixed,
+                            cls_capacity=N + steps)
+    outs = []
+    for rec, new_cls, _ in m.trace["steps"]:
+        qs, ks, vs = (x.double().cpu().numpy() for x in rec[li])
+        outs.append(O.decode_session_step(sess, qs, ks, vs, new_cls.cpu().numpy().astype(np.int64)))
+    return sess, outs
+
+
+@pytest.mark.parametrize("mode", ["adaptive", "fixed"])
+def test_llama_layers_match_oracle(mode):
+    from paper_2310_01801_b200 import ProfilerConfig, parse_policy
+
+    torch.backends.cuda.matmul.allow_tf32 = False
+    cfg = _tiny(n_layers=3)
+    m = _model(cfg, seed=11)
+    m.record = True
+    B, N, D = 2, 96, 12
+    ids = _prompt(B, N, cfg.vocab, seed=5)
+    T = 0.6
+    if mode == "adaptive":
+        pc = ProfilerConfig(recovery_threshold=T)
+        pre = m.prefill(ids, pc, max_new_tokens=D)
+        fam, thr, fixed = O.default_family(), [T], None
+    else:
+        pol = parse_policy("special+punct+frequent(r_f=0.3)+local(r_l=0.3)")
+        pre = m.prefill(ids, fixed_policy=pol, max_new_tokens=D)
+        fam, thr, fixed = None, None, O.Member(O.ATOM_SPECIAL | O.ATOM_PUNCT | O.ATOM_FREQUENT |
+                                               O.ATOM_LOCAL, 0.3, 0.3)
+    for _ in range(D):
+        m.decode_step()
+    torch.cuda.synchronize()
+    m.check()
+    evicted_any = False
+    for li in range(cfg.n_layers):
+        sess, outs = _replay_layer(m, li, fam, thr, fixed, D)
+        res = pre.profiles[li]
+        near = res.near_threshold()[:, 0] if fixed is None else np.zeros(res.choice.shape[0], bool)
+        got_pos = m.caches[li].retained_positions()
+        for g, (st, prof) in enumerate(zip(sess.heads, sess.profiles)):
+            if near[g]:
+                continue
+            assert int(res.choice[g, 0]) == prof.choice[0], (li, g, res.recovery[g], prof.recoveries)
+            np.testing.assert_array_equal(np.sort(got_pos[g]), np.sort(st.positions),
+                                          err_msg=f"layer {li} head {g}")
+            evicted_any |= st.evictions > 0
+        for t, (_, _, o_all) in enumerate(m.trace["steps"]):
+            got = o_all[li].double().cpu().numpy()
+            ref = outs[t]
+            ok = ~near.reshape(B, -1)
+            scale = np.abs(ref).max()
+            np.testing.assert_allclose(got[ok], ref[ok], rtol=1e-4, atol=1e-4 * scale)
+    if mode == "fixed":
+        assert evicted_any
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_caller_kernels_vs_torch(dtype):
+    from paper_2310_01801_b200.llama import FastGenLlama
+
+    cfg = _tiny(n_layers=1)
+    m = FastGenLlama(cfg, dtype=dtype, seed=1, special_ids=SPECIAL, punct_ids=PUNCT,
+                     max_positions=64)
+    tol = 1e-5 if dtype == torch.float32 else 2e-2
+    g = torch.Generator(device="cuda").manual_seed(0)
+    rows, dm = 37, cfg.d_model
+    res = torch.randn(rows, dm, device="cuda", generator=g).to(dtype)
+    x = torch.randn(rows, dm, device="cuda", generator=g).to(dtype)
+    w = (1 + 0.1 * torch.randn(dm, device="cuda", generator=g)).to(dtype)
+    r0 = res.clone()
+    out = m._rmsnorm(res, w, x=x)
+    h = (r0.float() + x.float()).to(dtype).float()
+    ref = h * torch.rsqrt(h.pow(2).mean(-1, keepdim=True) + cfg.eps) * w.float()
+    assert torch.allclose(res.float(), h)
+    assert torch.allclose(out.float(), ref, rtol=tol, atol=tol)
+    # rope scatter: T = B*n tokens at positions pos0..pos0+n-1
+    B, n, pos0, d, H = 3, 5, 7, cfg.head_dim, cfg.n_heads
+    qkv = torch.randn(B * n, 3 * H * d, device="cuda", generator=g).to(dtype)
+    q = torch.empty(B, H, n, d, dtype=dtype, device="cuda")
+    k, v = torch.empty_like(q), torch.empty_like(q)
+    m._rope(qkv, n, pos0, q, k, v, n)
+    xr = qkv.float().view(B, n, 3, H, d)
+    c = m.cos[pos0:pos0 + n][None, :, None, :]
+    s = m.sin[pos0:pos0 + n][None, :, None, :]
+
+    def rope(t):
+        t1, t2 = t[..., : d // 2], t[..., d // 2:]
+        return torch.cat([t1 * c - t2 * s, t2 * c + t1 * s], -1).transpose(1, 2)
+
+    assert torch.allclose(q.float(), rope(xr[:, :, 0]), rtol=tol, atol=tol)
+    assert torch.allclose(k.float(), rope(xr[:, :, 1]), rtol=tol, atol=tol)
+    assert torch.equal(v.float(), xr[:, :, 2].transpose(1, 2))
+    # swiglu
+    gu = torch.randn(rows, 2 * cfg.ffn, device="cuda", generator=g).to(dtype)
+    sw = m._swiglu(gu).float()
+    gf, uf = gu.float()[:, : cfg.ffn], gu.float()[:, cfg.ffn:]
+    assert torch.allclose(sw, torch.nn.functional.silu(gf) * uf, rtol=tol, atol=tol)
+    # greedy next: first-index argmax, class, embedding row
+    logits = torch.randn(4, cfg.vocab, device="cuda", generator=g).to(dtype)
+    logits[2, 10] = logits[2, 300] = logits[2].max() + 1  # tie -> lower index
+    logits[3, 7] = logits[3].max() + 1  # punct id
+    m.next_tok = torch.empty(4, dtype=torch.int64, device="cuda")
+    m.next_cls = torch.empty(4, dtype=torch.uint8, device="cuda")
+    m.x_next = torch.empty(4, dm, dtype=dtype, device="cuda")
+    m._greedy(logits)
+    ref_tok = torch.from_numpy(np.argmax(logits.float().cpu().numpy(), axis=1)).cuda()
+    assert torch.equal(m.next_tok, ref_tok)
+    assert int(m.next_tok[2]) == 10 and int(m.next_cls[3]) == 2
+    assert torch.equal(m.next_cls, m.lut[ref_tok])
+    assert torch.equal(m.x_next, m.embed[ref_tok])
