@@ -145,7 +145,7 @@ def run_session(w, T, qd, kd, vd, cd, slopes, sinks, decode_inputs, ev=None, rec
     for t in range(w.D):
         if record:
             lives.append(cache.live.cpu().numpy().copy())
-        decode_step_tensors(cache, dq[t], dk[t], dv[t], dc[t])
+        decode_step_tensors(cache, dq[t], dk[t], dv[t], dc[t], chained=True)
     if ev is not None:
         ev[2].record()
     if record:
@@ -376,7 +376,7 @@ def bench_e2e(w, T, args, qh, kh, vh, clsh, slopes, sinks, dev, dist):
         sv = step_views[slot]
         for t in range(D):
             q, k, v, c = sv[t]
-            decode_step_tensors(cache, q, k, v, c, out=out_views[t])
+            decode_step_tensors(cache, q, k, v, c, out=out_views[t], chained=True)
             if (t + 1) % CH == 0 or t + 1 == D:
                 c0 = (t // CH) * CH
                 e = chunk_done[t // CH]

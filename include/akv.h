@@ -189,7 +189,18 @@ typedef struct akv_decode_args {
   int64_t total_slots;           /* arena slots (sizes the logit scratch) */
   void* workspace_dev;
   size_t workspace_bytes;
+  const int32_t* pos_dev;        /* optional device position of the inserted token; when set it
+                                    replaces pos (so a captured CUDA graph can be replayed for
+                                    successive steps) */
+  int32_t flags;                 /* AKV_DECODE_* */
 } akv_decode_args;
+
+/* akv_decode_args.flags: the previous kernel on the stream is this cache's
+ * previous decode step and q/k/v/new_cls were complete before it started, so
+ * the step may stream settled full-cache pages before that kernel drains
+ * (programmatic dependent launch).  Without it the step waits for its
+ * predecessor before reading anything. */
+#define AKV_DECODE_CHAINED 1
 
 size_t akv_decode_workspace_size(int32_t B, int32_t H, int32_t d, int32_t max_cap, int64_t total_slots);
 int akv_decode_step(const akv_decode_args* a, void* stream);
@@ -278,6 +289,8 @@ typedef struct akv_rope_args {
   void* v_dev;
   int64_t out_ld;
   int32_t row0;
+  const int32_t* pos_dev;     /* optional device base added to pos0 (graph replays); positions
+                                 past the table are clamped to its last row */
 } akv_rope_args;
 /* rotate-half RoPE of q and k, copy of v, scattered head-major */
 int akv_rope_scatter(const akv_rope_args* a, void* stream);

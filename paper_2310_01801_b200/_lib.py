@@ -20,6 +20,7 @@ ROWS_ALL, ROWS_LAST = 0, 1
 CRIT_RECOVERY, CRIT_COSINE = 0, 1
 MAX_FAMILY = 8
 MAX_THRESHOLDS = 8
+DECODE_CHAINED = 1
 
 P = C.c_void_p
 i32, i64, f64, sz = C.c_int32, C.c_int64, C.c_double, C.c_size_t
@@ -64,6 +65,7 @@ class DecodeArgs(C.Structure):
         ("vc_dev", P), ("meta_dev", P), ("score_dev", P), ("base_live_dev", P), ("live_in_dev", P),
         ("live_out_dev", P), ("out_dev", P), ("evicted_dev", P), ("status_dev", P),
         ("max_cap", i32), ("total_slots", i64), ("workspace_dev", P), ("workspace_bytes", sz),
+        ("pos_dev", P), ("flags", i32),
     ]
 
 
@@ -80,6 +82,7 @@ class RopeArgs(C.Structure):
         ("T", i32), ("n", i32), ("Hl", i32), ("d", i32), ("dtype", i32), ("qkv_dev", P),
         ("qkv_ld", i64), ("pos0", i32), ("max_pos", i32), ("cos_dev", P), ("sin_dev", P),
         ("q_dev", P), ("k_dev", P), ("v_dev", P), ("out_ld", i64), ("row0", i32),
+        ("pos_dev", P),
     ]
 
 

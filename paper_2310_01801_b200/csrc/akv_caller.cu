@@ -132,7 +132,8 @@ __global__ void __launch_bounds__(128) k_rope_scatter(akv_rope_args a) {
   const int c = threadIdx.x % half;
   if (h >= a.Hl) return;
   const int b = t / a.n, i = t % a.n;
-  const int pos = a.pos0 + i;
+  int pos = a.pos0 + i + (a.pos_dev ? *a.pos_dev : 0);
+  pos = pos < a.max_pos ? pos : a.max_pos - 1;
   const T* row = reinterpret_cast<const T*>(a.qkv_dev) + (int64_t)t * a.qkv_ld;
   const int64_t hd = (int64_t)a.Hl * a.d;
   const float cs = a.cos_dev[(int64_t)pos * half + c];
@@ -286,7 +287,7 @@ extern "C" int akv_rope_scatter(const akv_rope_args* a, void* stream) {
     return set_error(AKV_ERR_INVALID, "akv_rope_scatter: bad arguments");
   if (a->d < 2 || a->d % 2 || 128 % (a->d / 2) || a->d > 256)
     return set_error(AKV_ERR_UNSUPPORTED, "akv_rope_scatter: head dim %d", a->d);
-  if (a->pos0 < 0 || a->pos0 + a->n > a->max_pos)
+  if (a->pos0 < 0 || (!a->pos_dev && a->pos0 + a->n > a->max_pos))
     return set_error(AKV_ERR_INVALID, "akv_rope_scatter: positions %d..%d out of range for a "
                      "%d-position table", a->pos0, a->pos0 + a->n - 1, a->max_pos);
   if (a->T == 0) return AKV_OK;

@@ -87,6 +87,8 @@ struct DecParams {
   int max_parts;
   float scale;
   unsigned long long* trace;  // optional [grid, 8] globaltimer stamps (AKV_DEC_TRACE)
+  const int32_t* pos_dev;     // device position (CUDA-graph replays), overrides pos
+  int flags;                  // AKV_DECODE_* flags
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -107,6 +109,7 @@ __device__ __forceinline__ int page_owner(long long pg, long long P, int grid) {
 
 struct HeadCtx {
   int g, L, n;
+  int pos;  // position of the inserted token
   int64_t base;
   uint8_t atoms;
   bool freq;
@@ -125,6 +128,7 @@ __device__ __forceinline__ void load_head(const DecParams& p, int g, int L, Head
   hc.slope = p.slope ? p.slope[h] : 0.f;
   hc.sink = p.sink ? p.sink[h] : 0.f;
   hc.ncls = p.new_cls[g / p.H];
+  hc.pos = p.pos_dev ? *p.pos_dev : p.pos;
 }
 
 __device__ __forceinline__ float biased_logit(float dot, int mt, const HeadCtx& hc, int pos) {
@@ -236,7 +240,7 @@ __device__ void policy_v3(const DecParams& p, const HeadCtx& hc, float lse, int*
   constexpr int NC = CS::kThreads, NW = CS::kWarps;
   const int tid = CS::tid(), lane = tid & 31, warp = tid >> 5;
   const int g = hc.g, L = hc.L, n = hc.n;
-  const int cur = p.pos + 1;
+  const int cur = hc.pos + 1;
   double* score = p.score + hc.base;
   int32_t* meta = p.meta + hc.base;
   const float* lg = p.logit + hc.base;
@@ -778,7 +782,7 @@ __global__ void __launch_bounds__(SimtShape<T, D>::NW * 32 + 32, 2) k3_decode_si
       uint4 kv;
       int mt;
       if (slot < L) { kv = kpage[row * LPR + sl]; mt = mpage[row]; }
-      else if (slot == L) { kv = hdr[LPR + sl]; mt = p.pos | (hc.ncls << kClsShift); }
+      else if (slot == L) { kv = hdr[LPR + sl]; mt = hc.pos | (hc.ncls << kClsShift); }
       else { kv = make_uint4(0, 0, 0, 0); mt = -1; }
       float kf[EV];
       Elem<T>::unpack(kv, kf);
@@ -789,7 +793,7 @@ __global__ void __launch_bounds__(SimtShape<T, D>::NW * 32 + 32, 2) k3_decode_si
       for (int off = 1; off < LPR; off <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
       float x = -INFINITY;
       if (mt >= 0) {
-        x = biased_logit(dot, mt, hc, p.pos);
+        x = biased_logit(dot, mt, hc, hc.pos);
         if (hc.freq && sl == 0 && slot < L) p.logit[hc.base + slot] = x;
       }
       sj[s] = x;
@@ -822,7 +826,7 @@ __global__ void __launch_bounds__(SimtShape<T, D>::NW * 32 + 32, 2) k3_decode_si
           st_v4(kw + sl, hdr[LPR + sl]);
           st_v4(vw + sl, vv);
           if (sl == 0) {
-            p.meta[hc.base + slot] = p.pos | (hc.ncls << kClsShift);
+            p.meta[hc.base + slot] = hc.pos | (hc.ncls << kClsShift);
             p.score[hc.base + slot] = 0.0;  // policies.py:357
           }
         }
@@ -944,9 +948,20 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
   // before griddepcontrol.wait.  Anything the previous step writes (its
   // inserted row, live counts and rows of evicting heads, semaphores,
   // partials, outputs) is touched only after the wait.
-  const int step = p.pos - p.prompt_len;
-  const bool early = step > 0;
-  if (!early) grid_dep_wait();
+  // Early streaming is opt-in (AKV_DECODE_CHAINED): the caller guarantees
+  // that q/k/v and the new classes were not written by the kernel launched
+  // just before this one (e.g. a rope kernel of a model layer).  A device
+  // position (graph replays) is read only after the wait.
+  int step;
+  bool early = false;
+  if (p.pos_dev) {
+    grid_dep_wait();
+    step = *p.pos_dev - p.prompt_len;
+  } else {
+    step = p.pos - p.prompt_len;
+    early = (p.flags & AKV_DECODE_CHAINED) && step > 0;
+    if (!early) grid_dep_wait();
+  }
   const long long P = plan_pages_bound(p, PAGE, step, s_prefix, s_live, s_full, red_i);
   AKV_TRACE(1);
   const int grid = (int)(P < (long long)gridDim.x ? P : (long long)gridDim.x);
@@ -1076,7 +1091,7 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
         st_v4(dstg + cc, val);  // fused insert into the arena
       }
       if (lane == 0) {
-        p.meta[hc.base + L] = p.pos | (hc.ncls << kClsShift);
+        p.meta[hc.base + L] = hc.pos | (hc.ncls << kClsShift);
         p.score[hc.base + L] = 0.0;  // policies.py:357
       }
       fence_proxy_async_smem();  // generic writes precede the next TMA into this stage
@@ -1113,8 +1128,8 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
         const int slot = slot0 + row;
         float x = -INFINITY;
         if (qq == 0 && slot < n) {
-          const int mt = slot < L ? mpage[row] : (p.pos | (hc.ncls << kClsShift));
-          x = biased_logit(acc[2 * h2] * p.scale, mt, hc, p.pos);
+          const int mt = slot < L ? mpage[row] : (hc.pos | (hc.ncls << kClsShift));
+          x = biased_logit(acc[2 * h2] * p.scale, mt, hc, hc.pos);
           if (hc.freq && slot < L) p.logit[hc.base + slot] = x;
         }
         sx[t][h2] = x;
@@ -1254,16 +1269,30 @@ struct TmapCache {
   int d = 0;
   CUtensorMap k, v;
 };
-static thread_local TmapCache g_tmaps;
+constexpr int kTmapSlots = 256;  // one per (layer) cache of a multi-layer model
+static thread_local TmapCache g_tmap_slots[kTmapSlots];
+static thread_local int g_tmap_next = 0;
+
+static TmapCache* tmap_lookup(const void* kc, const void* vc, int64_t slots, int d) {
+  for (int i = 0; i < kTmapSlots; ++i) {
+    TmapCache& c = g_tmap_slots[i];
+    if (c.kc == kc && c.vc == vc && c.slots == slots && c.d == d) return &c;
+  }
+  return nullptr;
+}
 
 template <int D>
 static cudaError_t launch_mma(const DecParams& p, int64_t total_slots, cudaStream_t st) {
   using S = MmaShape<D>;
-  if (g_tmaps.kc != p.kc || g_tmaps.vc != p.vc || g_tmaps.slots != total_slots || g_tmaps.d != D) {
-    if (!encode_tmap_2d_bf16(&g_tmaps.k, p.kc, (uint64_t)total_slots, D, 64, S::PAGE, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !encode_tmap_2d_bf16(&g_tmaps.v, p.vc, (uint64_t)total_slots, D, 64, S::PAGE, CU_TENSOR_MAP_SWIZZLE_128B))
+  TmapCache* tm = tmap_lookup(p.kc, p.vc, total_slots, D);
+  if (!tm) {
+    tm = &g_tmap_slots[g_tmap_next];
+    g_tmap_next = (g_tmap_next + 1) % kTmapSlots;
+    tm->kc = nullptr;
+    if (!encode_tmap_2d_bf16(&tm->k, p.kc, (uint64_t)total_slots, D, 64, S::PAGE, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !encode_tmap_2d_bf16(&tm->v, p.vc, (uint64_t)total_slots, D, 64, S::PAGE, CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
-    g_tmaps.kc = p.kc; g_tmaps.vc = p.vc; g_tmaps.slots = total_slots; g_tmaps.d = D;
+    tm->kc = p.kc; tm->vc = p.vc; tm->slots = total_slots; tm->d = D;
   }
   auto kern = k3_decode_mma<D>;
   static bool attr = false;
@@ -1277,7 +1306,7 @@ static cudaError_t launch_mma(const DecParams& p, int64_t total_slots, cudaStrea
   int sms;
   if ((e = num_sms(&sms))) return e;
   const size_t smem = 1024 + (size_t)kStages * S::STAGE_B + (size_t)(2 * p.G + 1) * 4 + p.G;
-  return launch_pdl(kern, 2 * sms, S::THREADS, smem, st, p, g_tmaps.k, g_tmaps.v);
+  return launch_pdl(kern, 2 * sms, S::THREADS, smem, st, p, tm->k, tm->v);
 }
 
 struct DecWs {
@@ -1341,8 +1370,10 @@ extern "C" int akv_decode_step(const akv_decode_args* a, void* stream) {
   if (a->B < 1 || a->H < 1) return set_error(AKV_ERR_INVALID, "akv_decode_step: empty input");
   if (a->B * a->H > kMaxHeads)
     return set_error(AKV_ERR_UNSUPPORTED, "akv_decode_step: more than %d heads per launch", kMaxHeads);
-  if (a->pos < a->prompt_len || a->prompt_len < 1)
+  if ((!a->pos_dev && a->pos < a->prompt_len) || a->prompt_len < 1)
     return set_error(AKV_ERR_INVALID, "akv_decode_step: need pos >= prompt_len >= 1");
+  if (a->pos_dev && (a->flags & AKV_DECODE_CHAINED))
+    return set_error(AKV_ERR_INVALID, "akv_decode_step: AKV_DECODE_CHAINED needs a host position");
   if (a->pos > kPosMask) return set_error(AKV_ERR_UNSUPPORTED, "akv_decode_step: position too large");
   if (a->live_in_dev == a->live_out_dev)
     return set_error(AKV_ERR_INVALID, "akv_decode_step: live_in and live_out must be distinct buffers");
@@ -1355,7 +1386,7 @@ extern "C" int akv_decode_step(const akv_decode_args* a, void* stream) {
               a->meta_dev, a->score_dev, a->base_live_dev, a->live_in_dev, a->live_out_dev,
               a->out_dev,
               a->evicted_dev, a->status_dev ? a->status_dev : w.status, w.part, w.logit, w.counter,
-              w.max_parts, (float)(1.0 / sqrt((double)a->d)), g_dec_trace};
+              w.max_parts, (float)(1.0 / sqrt((double)a->d)), g_dec_trace, a->pos_dev, a->flags};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaErrorInvalidValue;
   bool ok = true;

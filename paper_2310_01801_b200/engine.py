@@ -381,13 +381,19 @@ def _decode_args(cache: CompressedCache, dt: int) -> DecodeArgs:
     return a
 
 
-def decode_step_tensors(cache: CompressedCache, q, k, v, new_classes, out=None) -> torch.Tensor:
+def decode_step_tensors(cache: CompressedCache, q, k, v, new_classes, out=None, *,
+                        chained: bool = False) -> torch.Tensor:
     """One decode step for every head (Alg. 2 inner loop, engine.py:303-350):
     insert the new token's k/v, attend, update scores, evict.  q, k, v:
     CUDA tensors whose [B, H, :d] slices are the new token's rows (any
     head stride); new_classes: CUDA uint8 [B].  Returns the fp32 attention
     output [B, H, d]: ``out`` if given (contiguous fp32), else the cache's
-    pending-output buffer (overwritten by the next step)."""
+    pending-output buffer (overwritten by the next step).
+
+    ``chained=True`` promises that q/k/v/new_classes were not produced by the
+    kernel launched just before on this stream (they were resident, or
+    uploaded by a copy), which lets the step stream settled cache pages
+    while the previous step drains (AKV_DECODE_CHAINED)."""
     if cache.seq_len - cache.prompt_len >= cache.capacity_steps:
         raise EngineError(
             f"cache capacity of {cache.capacity_steps} decode steps exhausted; "
@@ -401,10 +407,39 @@ def decode_step_tensors(cache: CompressedCache, q, k, v, new_classes, out=None) 
     a.live_out_dev = _ptr(cache.live_buf[cache._parity ^ 1])
     dst = cache.out if out is None else out
     a.out_dev = _ptr(dst)
+    a.pos_dev = None
+    a.flags = _lib.DECODE_CHAINED if chained else 0
     check(lib.akv_decode_step(C.byref(a), _stream()), EngineError)
     cache._parity ^= 1
     cache.seq_len += 1
     return dst
+
+
+def decode_step_launch(cache: CompressedCache, q, k, v, new_classes, out, parity: int, pos_dev):
+    """Launch one decode step whose insert position is read from the device
+    (int32 ``pos_dev``) and whose live-count buffers are those of ``parity``,
+    without touching the host bookkeeping: the building block of a captured
+    CUDA graph that is replayed for successive steps.  The caller advances
+    ``pos_dev`` and, per replay, calls ``advance_host_state``."""
+    a = cache._dargs
+    a.pos = cache.prompt_len
+    a.q_dev, a.k_dev, a.v_dev = _ptr(q), _ptr(k), _ptr(v)
+    a.bh_stride = q.stride(1)
+    a.new_cls_dev = _ptr(new_classes)
+    a.live_in_dev = _ptr(cache.live_buf[parity])
+    a.live_out_dev = _ptr(cache.live_buf[parity ^ 1])
+    a.out_dev = _ptr(out)
+    a.pos_dev = _ptr(pos_dev)
+    a.flags = 0
+    check(lib.akv_decode_step(C.byref(a), _stream()), EngineError)
+    return out
+
+
+def advance_host_state(cache: CompressedCache):
+    """Host bookkeeping of one replayed decode step (see decode_step_launch);
+    the caller has checked the capacity before the replay."""
+    cache._parity ^= 1
+    cache.seq_len += 1
 
 
 # ---------------------------------------------------------------------------

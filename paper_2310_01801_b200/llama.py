@@ -46,7 +46,8 @@ import torch
 
 from . import _lib
 from ._lib import DTYPE_BF16, DTYPE_F32, RopeArgs, check, lib
-from .engine import EngineError, decode_step_tensors, encode_prompt_tensors
+from .engine import (EngineError, advance_host_state, decode_step_launch, decode_step_tensors,
+                     encode_prompt_tensors)
 from .parallel import all_reduce_partial, gather_head_blocks, shard_layer_weights
 from .profiler import ProfilerConfig
 from .workloads import PUNCT_IDS, SPECIAL_IDS, class_lut
@@ -164,6 +165,9 @@ class FastGenLlama:
         self._init_weights(seed)
         self.caches: list = []
         self.record = False
+        self.use_graphs = True
+        self._graphs = None
+        self.pos_dev = None
         self.trace: dict = {}
 
     # -- weights ------------------------------------------------------------
@@ -209,7 +213,7 @@ class FastGenLlama:
                                   self.cfg.eps, _ptr(out), _stream()), EngineError)
         return out
 
-    def _rope(self, qkv, n, pos0, q, k, v, out_ld):
+    def _rope(self, qkv, n, pos0, q, k, v, out_ld, pos_dev=None):
         a = RopeArgs()
         a.T, a.n, a.Hl, a.d, a.dtype = qkv.shape[0], n, self.Hl, self.cfg.head_dim, self.dt
         a.qkv_dev, a.qkv_ld = _ptr(qkv), qkv.stride(0)
@@ -217,6 +221,7 @@ class FastGenLlama:
         a.cos_dev, a.sin_dev = _ptr(self.cos), _ptr(self.sin)
         a.q_dev, a.k_dev, a.v_dev = _ptr(q), _ptr(k), _ptr(v)
         a.out_ld, a.row0 = out_ld, 0
+        a.pos_dev = _ptr(pos_dev)
         check(lib.akv_rope_scatter(C.byref(a), _stream()), EngineError)
 
     def _swiglu(self, gu):
@@ -285,6 +290,7 @@ class FastGenLlama:
         q = torch.empty(B, self.Hl, N, d, dtype=self.dtype, device=self.device)
         k, v = torch.empty_like(q), torch.empty_like(q)
         self.caches, profiles, prof_events = [], [], []
+        self._graphs = None
         self.trace = {"prompt": [], "steps": []} if self.record else {}
         delta = None
         for li, L in enumerate(self.layers):
@@ -329,27 +335,49 @@ class FastGenLlama:
     def decode_step(self) -> torch.Tensor:
         """Insert the pending token of every sequence into every layer's
         compressed cache and produce the next one (greedy).  Returns the
-        inserted tokens [B] (device, int64; a copy)."""
+        inserted tokens [B] (device, int64; a copy).
+
+        Unless ``record`` is set or ``use_graphs`` is off, the first step
+        runs eagerly and captures the whole step (every layer's kernels and
+        GEMMs) into two CUDA graphs - one per parity of the double-buffered
+        live counts - whose K3 and RoPE launches read the insert position
+        from the device; later steps are graph replays."""
         if not self.caches:
             raise EngineError("decode_step before prefill")
         if self.seq_len - self.N >= self.capacity:
             raise EngineError(f"cache capacity of {self.capacity} decode steps exhausted")
-        cfg, d, B = self.cfg, self.cfg.head_dim, self.B
-        pos = self.seq_len
-        inserted = self.next_tok.clone()
-        new_cls = self.next_cls.clone()
-        self.classes[:, pos] = new_cls
-        residual = self.x_next.clone()
+        if self.record or not self.use_graphs:
+            return self._step_eager()
+        if self._graphs is None:
+            out = self._step_eager()
+            self._capture()
+            return out
+        parity = self.caches[0]._parity
+        self._graphs[parity].replay()
+        self.last_logits = self._graph_logits[parity]
+        for c in self.caches:
+            advance_host_state(c)
+        self.seq_len += 1
+        return self.ins_buf.clone()
+
+    def _layers_step(self, residual, new_cls, pos=None, parity=None, rec=None):
+        """Every layer of one decode step; host ``pos`` (eager, through
+        decode_step_tensors) or the device position (graph capture)."""
+        d, B = self.cfg.head_dim, self.B
         delta = None
-        rec = [] if self.record else None
         for li, L in enumerate(self.layers):
             xn = self._rmsnorm(residual, L.attn_norm, x=delta)
             qkv = torch.nn.functional.linear(xn, L.wqkv)
-            self._rope(qkv, 1, pos, self.q1, self.k1, self.v1, 1)
-            if rec is not None:
-                rec.append((self.q1.clone(), self.k1.clone(), self.v1.clone()))
-            o = decode_step_tensors(self.caches[li], self.q1, self.k1, self.v1, new_cls,
-                                    out=self.o_dec[li])
+            if pos is None:
+                self._rope(qkv, 1, 0, self.q1, self.k1, self.v1, 1, pos_dev=self.pos_dev)
+                o = decode_step_launch(self.caches[li], self.q1, self.k1, self.v1, new_cls,
+                                       self.o_dec[li], parity, self.pos_dev)
+            else:
+                self._rope(qkv, 1, pos, self.q1, self.k1, self.v1, 1)
+                if rec is not None:
+                    rec.append((self.q1.clone(), self.k1.clone(), self.v1.clone()))
+                o = decode_step_tensors(self.caches[li], self.q1, self.k1, self.v1, new_cls,
+                                        out=self.o_dec[li])
             o = self._gather_heads(o.view(B, self.Hl * d).to(self.dtype))
             attn = self._reduce(torch.nn.functional.linear(o, L.wo))
             delta = self._mlp(L, residual, attn)
@@ -357,10 +385,51 @@ class FastGenLlama:
         logits = torch.nn.functional.linear(xf, self.lm_head)
         self._greedy(logits)
         self.last_logits = logits
+
+    def _step_eager(self) -> torch.Tensor:
+        pos = self.seq_len
+        inserted = self.next_tok.clone()
+        new_cls = self.next_cls.clone()
+        self.classes[:, pos] = new_cls
+        rec = [] if self.record else None
+        self._layers_step(self.x_next.clone(), new_cls, pos=pos, rec=rec)
         if rec is not None:
             self.trace["steps"].append((rec, new_cls.clone(), self.o_dec.clone()))
         self.seq_len += 1
         return inserted
+
+    def _capture(self):
+        """Capture one decode step per live-count parity (see decode_step).
+        The graph snapshots the pending token / class / embedding row, runs
+        every layer, picks the next token and advances the device position."""
+        self.pos_dev = torch.full((1,), self.seq_len, dtype=torch.int32, device=self.device)
+        # every buffer a captured graph touches must outlive the graphs
+        self.ins_buf = torch.empty_like(self.next_tok)
+        cls_buf = self._g_cls = torch.empty_like(self.next_cls)
+        res_buf = self._g_res = torch.empty_like(self.x_next)
+        col = self._g_col = torch.empty(1, dtype=torch.int64, device=self.device)
+        parity0 = self.caches[0]._parity
+        if any(c._parity != parity0 for c in self.caches):
+            raise EngineError("layer caches out of step")
+        torch.cuda.synchronize()
+        graphs, self._graph_logits = {}, {}
+        eager_logits = self.last_logits
+        pool = None
+        for parity in (parity0, parity0 ^ 1):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, pool=pool):
+                self.ins_buf.copy_(self.next_tok)
+                cls_buf.copy_(self.next_cls)
+                res_buf.copy_(self.x_next)
+                col.copy_(self.pos_dev)
+                self.classes.index_copy_(1, col, cls_buf[:, None])
+                self._layers_step(res_buf, cls_buf, parity=parity)
+                self.pos_dev.add_(1)
+            pool = g.pool()
+            graphs[parity] = g
+            self._graph_logits[parity] = self.last_logits
+        self.last_logits = eager_logits
+        self._graphs = graphs
 
     def generate(self, tokens, profiler_cfg=None, max_new_tokens: int = 16, fixed_policy=None):
         """Prefill then ``max_new_tokens`` greedy tokens; returns [B, D]

@@ -57,10 +57,11 @@ def run_arrays(q, k, v, cls, N, D, slopes, sinks, cfg=None, fixed=None, extra=()
     out["lastrow"] = cache.lastp.cpu().numpy().astype(np.float64)
     dec_kept = np.zeros((D, G, N + D), bool)
     dec_out = np.zeros((D, G, d))
+    cls_cols = [ct[:, N + t].contiguous() for t in range(D)]
     for t in range(D):
         pos = N + t
         o = decode_step_tensors(cache, qt[:, :, pos], kt[:, :, pos], vt[:, :, pos],
-                                ct[:, pos].contiguous())
+                                cls_cols[t], chained=True)
         if record_steps:
             dec_out[t] = o.reshape(G, d).cpu().numpy()
             for g, p in enumerate(cache.retained_positions()):

@@ -38,7 +38,7 @@ def main():
     for _ in range(2):  # warm
         c = enc()
         for t in range(D):
-            decode_step_tensors(c, dq[t], dk[t], dv[t], dc[t])
+            decode_step_tensors(c, dq[t], dk[t], dv[t], dc[t], chained=True)
     torch.cuda.synchronize()
     # eager
     c = enc()
@@ -47,7 +47,7 @@ def main():
     h0 = time.perf_counter()
     e0.record()
     for t in range(D):
-        decode_step_tensors(c, dq[t], dk[t], dv[t], dc[t])
+        decode_step_tensors(c, dq[t], dk[t], dv[t], dc[t], chained=True)
     e1.record()
     h1 = time.perf_counter()
     torch.cuda.synchronize()
@@ -62,7 +62,7 @@ def main():
     with torch.cuda.stream(s):
         with torch.cuda.graph(g, stream=s):
             for t in range(D):
-                decode_step_tensors(c, dq[t], dk[t], dv[t], dc[t])
+                decode_step_tensors(c, dq[t], dk[t], dv[t], dc[t], chained=True)
     torch.cuda.current_stream().wait_stream(s)
     torch.cuda.synchronize()
     e0.record()

@@ -41,7 +41,7 @@ for s in range(20):
     t1 = time.perf_counter()
     calls = marks["calls"]
     for t in range(D):
-        decode_step_tensors(c, *dec[t])
+        decode_step_tensors(c, *dec[t], chained=True)
     t2 = time.perf_counter()
     # calls: profile, plan, compact, ws_init ; phases between them
     rows.append((calls[0] - t0, calls[1] - calls[0], calls[2] - calls[1], calls[3] - calls[2],

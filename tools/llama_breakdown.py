@@ -70,3 +70,51 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def decode_breakdown(B=16, N=2048, steps=20):
+    """Per-op time of one decode layer step (1-layer model, c2 shapes)."""
+    from paper_2310_01801_b200 import decode_step_tensors
+
+    cfg = type(LLAMA_7B)(**{**LLAMA_7B.__dict__, "n_layers": 1})
+    m = FastGenLlama(cfg, max_positions=N + 600)
+    ids = torch.randint(0, cfg.vocab, (B, N), device="cuda")
+    m.prefill(ids, ProfilerConfig(recovery_threshold=0.95), max_new_tokens=512)
+    for _ in range(3):
+        m.decode_step()
+    L = m.layers[0]
+    d = cfg.head_dim
+    res = m.x_next.clone()
+    print(f"decode B={B} L~{N}")
+    xn = timed("rmsnorm", lambda: m._rmsnorm(res, L.attn_norm), reps=steps)
+    qkv = timed("qkv gemm", lambda: torch.nn.functional.linear(xn, L.wqkv), reps=steps)
+    timed("rope_scatter", lambda: m._rope(qkv, 1, m.seq_len, m.q1, m.k1, m.v1, 1), reps=steps)
+    c = m.caches[0]
+    cls = m.next_cls.clone()
+
+    def k3():
+        o = decode_step_tensors(c, m.q1, m.k1, m.v1, cls, out=m.o_dec[0])
+        return o
+    o = timed("K3 decode step", k3, reps=steps)
+    ob = timed("cast o", lambda: o.view(B, -1).to(torch.bfloat16), reps=steps)
+    attn = timed("o gemm", lambda: torch.nn.functional.linear(ob, L.wo), reps=steps)
+    xn2 = timed("add_rmsnorm", lambda: m._rmsnorm(res, L.mlp_norm, x=attn), reps=steps)
+    gu = timed("gate|up gemm", lambda: torch.nn.functional.linear(xn2, L.wgu), reps=steps)
+    sw = timed("swiglu", lambda: m._swiglu(gu), reps=steps)
+    timed("down gemm", lambda: torch.nn.functional.linear(sw, L.wdown), reps=steps)
+    logits = timed("lm_head gemm", lambda: torch.nn.functional.linear(xn2, m.lm_head), reps=steps)
+    timed("greedy_next", lambda: m._greedy(logits), reps=steps)
+    import time as _t
+    torch.cuda.synchronize()
+    t0 = _t.perf_counter()
+    for _ in range(steps):
+        m.decode_step()
+    t1 = _t.perf_counter()
+    torch.cuda.synchronize()
+    t2 = _t.perf_counter()
+    print(f"full 1-layer decode_step: host {1e3 * (t1 - t0) / steps:.3f} ms/step issue, "
+          f"{1e3 * (t2 - t0) / steps:.3f} ms/step wall")
+
+
+if __name__ == "__main__" and os.environ.get("DECODE", "1") == "1":
+    decode_breakdown()

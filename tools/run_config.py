@@ -29,6 +29,7 @@ from paper_2310_01801_b200.workloads import CONFIGS  # noqa: E402
 def session(w, T, qd, kd, vd, cd, sl, sk, record):
     N, D = w.N, w.D
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    cls_cols = [cd[:, N + t].contiguous() for t in range(D)]
     ev[0].record()
     res, c = encode_prompt_tensors(qd, kd, vd, cd, ProfilerConfig(recovery_threshold=T),
                                    prompt_len=N, max_new_tokens=D, slopes=sl, sinks=sk)
@@ -36,7 +37,7 @@ def session(w, T, qd, kd, vd, cd, sl, sk, record):
     outs, lives = [], []
     for t in range(D):
         o = decode_step_tensors(c, qd[:, :, N + t], kd[:, :, N + t], vd[:, :, N + t],
-                                cd[:, N + t].contiguous())
+                                cls_cols[t], chained=True)
         if record:
             outs.append(o.clone())
             lives.append(c.live.clone())
