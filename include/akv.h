@@ -209,6 +209,32 @@ int akv_decode_workspace_init(void* workspace_dev, size_t workspace_bytes, int32
                               int32_t d, int32_t max_cap, int64_t total_slots, void* stream);
 
 
+/* ---- diagnostics: per-step recovery against uncompressed attention -----
+ * Replaces engine.py:341-349 (shadow keys, full softmax of the new query,
+ * recovery = mass on the attended positions).  Launch BEFORE the decode step
+ * of the same position (live_in is the pre-eviction live set); it appends
+ * the new key to the shadow rows and the new class to cls_hist. */
+typedef struct akv_diag_args {
+  int32_t B, H, d, dtype;
+  int32_t pos;                   /* position of the new token (ignored when pos_dev is set) */
+  const int32_t* pos_dev;        /* optional device position (graph replays) */
+  const void* q_dev;             /* [B,H,d] rows of the new token, head stride bh_stride */
+  const void* k_dev;
+  int64_t bh_stride;
+  const uint8_t* new_cls_dev;    /* [B] */
+  const float* slope_dev;        /* [H] or NULL (planted bias, as in the decode step) */
+  const float* sink_dev;         /* [H] or NULL */
+  const int64_t* seg_off_dev;    /* the cache's segments, live counts and slot metadata */
+  const int32_t* live_in_dev;
+  const int32_t* meta_dev;
+  void* shadow_dev;              /* [B*H, shadow_ld, d] every key by position (in/out) */
+  int64_t shadow_ld;
+  uint8_t* cls_hist_dev;         /* [B, cls_ld] class of every position (in/out), or NULL */
+  int64_t cls_ld;
+  double* recovery_dev;          /* [B*H] out */
+} akv_diag_args;
+int akv_decode_recovery(const akv_diag_args* a, void* stream);
+
 /* ---- reference single-context operations (float64, batched) ----------
  * The reference's building blocks besides the fused session path, so the
  * Python mirror of attention.py / policies.py / profiler.py runs on the GPU.

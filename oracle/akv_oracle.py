@@ -206,6 +206,8 @@ class HeadState:
     slope: float = 0.0
     sink: float = 0.0
     evictions: int = 0
+    shadow: np.ndarray | None = None  # every key by position (diagnostics, engine.py:260-261)
+    recovery: float = 0.0             # last_row_recovery (engine.py:256-258, 348)
 
 
 def compact_head(res: HeadProfileResult, k, v, member: Member, n, slope, sink):
@@ -214,7 +216,8 @@ def compact_head(res: HeadProfileResult, k, v, member: Member, n, slope, sink):
     kept = res.kept
     scores = res.colsum.copy() if member.atoms & ATOM_FREQUENT else None
     return HeadState(member, kept.copy(), k[kept].copy(), v[kept].copy(), scores,
-                     res.out_last.copy(), slope, sink)
+                     res.out_last.copy(), slope, sink, shadow=k[:n].copy(),
+                     recovery=float(res.lastp[kept].sum()) if kept.size else 0.0)
 
 
 def decode_head(st: HeadState, q, k_new, v_new, pos, cls_pos, prompt_len):
@@ -250,6 +253,15 @@ def decode_head(st: HeadState, q, k_new, v_new, pos, cls_pos, prompt_len):
     st.K = K_att[sel]
     st.V = V_att[sel]
     st.out = out
+    if st.shadow is not None:              # engine.py:341-349
+        st.shadow = np.vstack([st.shadow, k_new[None, :]])
+        full = (st.shadow @ q) / np.sqrt(float(d))
+        allpos = np.arange(pos + 1)
+        if st.slope != 0.0:
+            full = full - st.slope * (pos - allpos)
+        if st.sink != 0.0:
+            full = full + st.sink * (cls_pos[allpos] == CLS_SPECIAL)
+        st.recovery = float(softmax_vector(full)[attended].sum())
     return out
 
 

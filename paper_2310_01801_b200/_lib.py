@@ -86,10 +86,21 @@ class RopeArgs(C.Structure):
     ]
 
 
+class DiagArgs(C.Structure):
+    _fields_ = [
+        ("B", i32), ("H", i32), ("d", i32), ("dtype", i32), ("pos", i32), ("pos_dev", P),
+        ("q_dev", P), ("k_dev", P), ("bh_stride", i64), ("new_cls_dev", P), ("slope_dev", P),
+        ("sink_dev", P), ("seg_off_dev", P), ("live_in_dev", P), ("meta_dev", P),
+        ("shadow_dev", P), ("shadow_ld", i64), ("cls_hist_dev", P), ("cls_ld", i64),
+        ("recovery_dev", P),
+    ]
+
+
 # every symbol include/akv.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "akv_profile_workspace_size", "akv_profile", "akv_compact", "akv_plan_segments",
     "akv_decode_workspace_size", "akv_decode_step", "akv_decode_workspace_init",
+    "akv_decode_recovery",
     "akv_softmax_rows_f64", "akv_causal_attention_f64", "akv_keep_mask", "akv_map_recovery_f64",
     "akv_update_scores_f64", "akv_gather_rows_f64", "akv_tv_distance_f64",
     "akv_embed_classify", "akv_add_rmsnorm", "akv_rope_scatter", "akv_swiglu",
@@ -124,6 +135,8 @@ def _load():
     lib.akv_update_scores_f64.argtypes = [i32, P, i32, P, P, P, P]
     lib.akv_gather_rows_f64.argtypes = [i32, i32, P, P, i32, P, P, P, P]
     lib.akv_tv_distance_f64.argtypes = [i32, P, P, P, P]
+    lib.akv_decode_recovery.argtypes = [C.POINTER(DiagArgs), P]
+    lib.akv_decode_recovery.restype = C.c_int
     lib.akv_embed_classify.argtypes = [i32, P, i32, P, P, i32, i32, P, P, P]
     lib.akv_add_rmsnorm.argtypes = [i32, i32, i32, P, P, P, C.c_float, P, P]
     lib.akv_rope_scatter.argtypes = [C.POINTER(RopeArgs), P]

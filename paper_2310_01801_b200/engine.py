@@ -204,7 +204,7 @@ def _family_arrays(family, args):
 def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None = None,
                           fixed_policy: CompressionPolicy | None = None, *, prompt_len=None,
                           max_new_tokens: int = 0, extra_thresholds=(), slopes=None,
-                          sinks=None):
+                          sinks=None, diagnostics: bool = False):
     """Profile, select and compact every head of a batch (Alg. 1,
     engine.py:203-272) on the GPU.
 
@@ -214,6 +214,11 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
     slopes/sinks: optional CUDA float32 [H] planted head bias (synthetic
     workloads).  Returns (ProfileResult, CompressedCache) with capacity for
     ``max_new_tokens`` inserted tokens per head.
+
+    ``diagnostics=True`` also keeps every key by position (the reference's
+    shadow keys, engine.py:260-261) so that each decode step reports the
+    recovery of its attended set against uncompressed attention
+    (``cache.step_recovery``, engine.py:341-349).
     """
     if profiler_cfg is None and fixed_policy is None:
         raise EngineError("need a profiler config or a fixed policy")
@@ -362,7 +367,35 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
     check(lib.akv_decode_workspace_init(_ptr(cache.workspace), ws_bytes, B, H, d, cache.max_cap,
                                         cache.total_slots, stream))
     cache._dargs = _decode_args(cache, dt)
+    cache.track_recovery = bool(diagnostics)
+    # per-head recovery of the latest step; before any decode step it is the
+    # prompt's last-row recovery (engine.py:256-258, 362-363)
+    cache.step_recovery = view(summary, "lrr")
+    if diagnostics:
+        cache.shadow = torch.empty(G, N + int(max_new_tokens), d, dtype=q.dtype, device=dev)
+        cache.shadow.view(B, H, -1, d)[:, :, :N].copy_(k[:, :, :N])
+        cache.cls_hist = torch.zeros(B, N + int(max_new_tokens), dtype=torch.uint8, device=dev)
+        cache.cls_hist[:, :N].copy_(classes[:, :N])
+        cache.step_recovery = cache.step_recovery.clone()
+        g = _lib.DiagArgs()
+        g.B, g.H, g.d, g.dtype = B, H, d, dt
+        g.slope_dev, g.sink_dev = _ptr(slopes), _ptr(sinks)
+        g.seg_off_dev, g.meta_dev = _ptr(cache.seg_off), _ptr(cache.meta)
+        g.shadow_dev, g.shadow_ld = _ptr(cache.shadow), cache.shadow.shape[1]
+        g.cls_hist_dev, g.cls_ld = _ptr(cache.cls_hist), cache.cls_hist.shape[1]
+        g.recovery_dev = _ptr(cache.step_recovery)
+        cache._diag_args = g
     return res, cache
+
+
+def _launch_recovery(cache, q, k, new_classes, live_in, pos=None, pos_dev=None):
+    g = cache._diag_args
+    g.pos = 0 if pos is None else pos
+    g.pos_dev = _ptr(pos_dev)
+    g.q_dev, g.k_dev, g.bh_stride = _ptr(q), _ptr(k), q.stride(1)
+    g.new_cls_dev = _ptr(new_classes)
+    g.live_in_dev = _ptr(live_in)
+    check(lib.akv_decode_recovery(C.byref(g), _stream()), EngineError)
 
 
 def _decode_args(cache: CompressedCache, dt: int) -> DecodeArgs:
@@ -409,6 +442,9 @@ def decode_step_tensors(cache: CompressedCache, q, k, v, new_classes, out=None, 
     a.out_dev = _ptr(dst)
     a.pos_dev = None
     a.flags = _lib.DECODE_CHAINED if chained else 0
+    if cache.track_recovery:
+        _launch_recovery(cache, q, k, new_classes, cache.live_buf[cache._parity], pos=cache.seq_len)
+        a.flags = 0  # the recovery kernel sits between two decode steps
     check(lib.akv_decode_step(C.byref(a), _stream()), EngineError)
     cache._parity ^= 1
     cache.seq_len += 1
@@ -431,6 +467,8 @@ def decode_step_launch(cache: CompressedCache, q, k, v, new_classes, out, parity
     a.out_dev = _ptr(out)
     a.pos_dev = _ptr(pos_dev)
     a.flags = 0
+    if cache.track_recovery:
+        _launch_recovery(cache, q, k, new_classes, cache.live_buf[parity], pos_dev=pos_dev)
     check(lib.akv_decode_step(C.byref(a), _stream()), EngineError)
     return out
 
@@ -500,7 +538,8 @@ def encode_prompt(model, prompt_tokens, profiler_cfg: ProfilerConfig | None,
     cls = torch.tensor([[CLASS_CODE[a.klass] for a in annotations]], dtype=torch.uint8)
     res, cache = encode_prompt_tensors(
         torch.from_numpy(q).to(dev), torch.from_numpy(k).to(dev), torch.from_numpy(v).to(dev),
-        cls.to(dev), profiler_cfg, fixed_policy, max_new_tokens=max_new_tokens)
+        cls.to(dev), profiler_cfg, fixed_policy, max_new_tokens=max_new_tokens,
+        diagnostics=diagnostics)
     choice = res.choice[:, 0]
     decisions = {}
     for gi, key in enumerate(grid):
@@ -548,7 +587,8 @@ def generate_step(model, cache: CompressedCache, last_token=None, sampler=None):
     cache.last_record = StepRecord(
         step=0, token_id=next_token,
         head_retained={key: int(live[i]) for i, key in enumerate(cache.keys)},
-        total_cache_tokens=int(live.sum()), mean_recovery=None,
+        total_cache_tokens=int(live.sum()),
+        mean_recovery=(float(cache.step_recovery.mean().item()) if cache.diagnostics else None),
         retained_positions=(
             {key: tuple(int(x) for x in p)
              for key, p in zip(cache.keys, cache.retained_positions())}

@@ -258,11 +258,15 @@ class FastGenLlama:
 
     # -- prefill ------------------------------------------------------------
     def prefill(self, tokens: torch.Tensor, profiler_cfg: ProfilerConfig | None = None,
-                max_new_tokens: int = 0, fixed_policy=None, extra_thresholds=()):
+                max_new_tokens: int = 0, fixed_policy=None, extra_thresholds=(),
+                diagnostics: bool = False):
         """Run the prompt ``tokens`` [B, N] (int64, device) through every
         layer: full causal attention for the prompt rows, K1 profiling and
         K2 compaction of each layer's heads.  Returns a PrefillResult; the
-        next token per sequence is left on the device for decode_step."""
+        next token per sequence is left on the device for decode_step.
+        ``diagnostics`` keeps every layer's shadow keys so that each decode
+        step also reports its heads' recovery against uncompressed attention
+        (``mean_recovery``; engine.py:341-349)."""
         cfg, d, dm = self.cfg, self.cfg.head_dim, self.cfg.d_model
         if tokens.dim() != 2 or not tokens.is_cuda:
             raise EngineError("tokens must be a CUDA tensor [B, N]")
@@ -304,7 +308,8 @@ class FastGenLlama:
             ev0.record()
             res, cache = encode_prompt_tensors(
                 q, k, v, cls_prompt, profiler_cfg, fixed_policy, prompt_len=N,
-                max_new_tokens=max_new_tokens, extra_thresholds=extra_thresholds)
+                max_new_tokens=max_new_tokens, extra_thresholds=extra_thresholds,
+                diagnostics=diagnostics)
             ev1 = torch.cuda.Event(enable_timing=True)
             ev1.record()
             prof_events.append((ev0, ev1))
@@ -439,6 +444,13 @@ class FastGenLlama:
         for t in range(max_new_tokens):
             out[:, t] = self.decode_step()
         return out
+
+    def mean_recovery(self) -> float:
+        """Mean over layers and heads of the latest step's recovery (the
+        reference's StepRecord.mean_recovery); needs prefill(diagnostics=True)."""
+        if not self.caches or not self.caches[0].track_recovery:
+            raise EngineError("mean_recovery needs prefill(..., diagnostics=True)")
+        return float(torch.stack([c.step_recovery for c in self.caches]).mean())
 
     def check(self):
         for c in self.caches:

@@ -147,17 +147,27 @@ def run_sequence(model, tokens, N, D, cfg_list, decode_cfg, fixed):
         enc_rec[gi] = prof[key].recovery
         dec_choice[gi] = list(fam).index(st.policy)
     generate_step(model, cache, None)
+    # diagnostics: per-head recovery vs the uncompressed shadow softmax
+    # (engine.py:341-349); row 0 is the first (sampling-only) step, whose
+    # recoveries are the prompt's last-row recoveries (engine.py:362-363)
+    dec_rec = np.zeros((D + 1, len(grid)))
+    dec_mean = np.zeros(D + 1)
+    dec_rec[0] = [cache.heads[key].last_row_recovery for key in grid]
+    dec_mean[0] = cache.last_record.mean_recovery
     dec_kept = np.zeros((D, len(grid), total), dtype=bool)
     dec_out = np.zeros((D, len(grid), model.v.shape[-1]))
     for t in range(D):
         generate_step(model, cache, int(tokens[N + t]))
         rec = cache.last_record.retained_positions
+        dec_mean[t + 1] = cache.last_record.mean_recovery
         for gi, key in enumerate(grid):
             dec_kept[t, gi, list(rec[key])] = True
             dec_out[t, gi] = cache.heads[key].pending_output
+            dec_rec[t + 1, gi] = cache.heads[key].last_row_recovery
     return dict(R=R, cost=cost, cos=cos, colsum=colsum, lastrow=lastrow, choice=choice,
                 csvs=csvs, enc_kept=enc_kept, enc_out=enc_out, enc_rec=enc_rec,
-                dec_choice=dec_choice, dec_kept=dec_kept, dec_out=dec_out,
+                dec_choice=dec_choice, dec_kept=dec_kept, dec_out=dec_out, dec_rec=dec_rec,
+                dec_mean=dec_mean,
                 family=np.array([atom_bits(p) for p in fam]))
 
 
@@ -186,6 +196,8 @@ def make_workload_case(name):
     out["dec_kept"] = np.packbits(np.concatenate([p["dec_kept"] for p in parts], axis=1), axis=-1)
     out["enc_kept"] = np.packbits(out["enc_kept"], axis=-1)
     out["dec_out"] = np.concatenate([p["dec_out"] for p in parts], axis=1)
+    out["dec_rec"] = np.concatenate([p["dec_rec"] for p in parts], axis=1)
+    out["dec_mean"] = np.stack([p["dec_mean"] for p in parts])  # [batch rows, D+1]
     out["family"] = parts[0]["family"]
     # CSV per threshold, one block per batch row (the reference grid is per sequence)
     out["csvs"] = np.array(["\n---\n".join(p["csvs"][i] for p in parts)
@@ -216,6 +228,8 @@ def make_mixed():
     tokens = list(prompt)
     dec_kept = np.zeros((S, len(grid), P + S), dtype=bool)
     dec_out = np.zeros((S, len(grid), 16))
+    dec_rec = np.zeros((S + 1, len(grid)))
+    dec_rec[0] = [cache.heads[key].last_row_recovery for key in grid]
     for t in range(S):
         tokens.append(tok)
         tok, _ = generate_step(model, cache, tokens[-1])
@@ -223,6 +237,7 @@ def make_mixed():
         for gi, key in enumerate(grid):
             dec_kept[t, gi, list(rec[key])] = True
             dec_out[t, gi] = cache.heads[key].pending_output
+            dec_rec[t + 1, gi] = cache.heads[key].last_row_recovery
     T = len(tokens)
     klass = [model.vocab.classify_id(t) for t in tokens]
     q = np.zeros((len(grid), T, 16))
@@ -240,7 +255,7 @@ def make_mixed():
         punct=np.array(sorted(model.vocab.punctuation_ids)),
         choice=choice, csv=np.array(prof.to_csv()),
         enc_kept=np.packbits(enc_kept, axis=-1), enc_out=enc_out,
-        dec_kept=np.packbits(dec_kept, axis=-1), dec_out=dec_out)
+        dec_kept=np.packbits(dec_kept, axis=-1), dec_out=dec_out, dec_rec=dec_rec)
 
 
 def main(argv):

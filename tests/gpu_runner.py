@@ -45,7 +45,7 @@ def run_arrays(q, k, v, cls, N, D, slopes, sinks, cfg=None, fixed=None, extra=()
     sk = None if sinks is None else torch.tensor(sinks, dtype=torch.float32, device=dev)
     res, cache = encode_prompt_tensors(qt, kt, vt, ct, cfg, fixed, prompt_len=N,
                                        max_new_tokens=D, extra_thresholds=extra, slopes=sl,
-                                       sinks=sk)
+                                       sinks=sk, diagnostics=True)
     G = B * H
     out = dict(res=res, cache=cache)
     enc_kept = np.zeros((G, N), bool)
@@ -57,6 +57,8 @@ def run_arrays(q, k, v, cls, N, D, slopes, sinks, cfg=None, fixed=None, extra=()
     out["lastrow"] = cache.lastp.cpu().numpy().astype(np.float64)
     dec_kept = np.zeros((D, G, N + D), bool)
     dec_out = np.zeros((D, G, d))
+    dec_rec = np.zeros((D + 1, G))
+    dec_rec[0] = cache.step_recovery.cpu().numpy()
     cls_cols = [ct[:, N + t].contiguous() for t in range(D)]
     for t in range(D):
         pos = N + t
@@ -64,12 +66,14 @@ def run_arrays(q, k, v, cls, N, D, slopes, sinks, cfg=None, fixed=None, extra=()
                                 cls_cols[t], chained=True)
         if record_steps:
             dec_out[t] = o.reshape(G, d).cpu().numpy()
+            dec_rec[t + 1] = cache.step_recovery.cpu().numpy()
             for g, p in enumerate(cache.retained_positions()):
                 dec_kept[t, g, p] = True
     torch.cuda.synchronize()
     cache.check()
     out["dec_kept"] = dec_kept
     out["dec_out"] = dec_out
+    out["dec_rec"] = dec_rec
     return out
 
 

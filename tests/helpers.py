@@ -59,7 +59,8 @@ def oracle_case(name):
     N, D = w.N, w.D
     res = dict(R=[], cost=[], choice=[], colsum=[], lastrow=[], enc_kept=[], enc_out=[],
                dec_kept=np.zeros((D, len(heads), N + D), bool),
-               dec_out=np.zeros((D, len(heads), w.d)), dec_choice=[])
+               dec_out=np.zeros((D, len(heads), w.d)), dec_choice=[],
+               dec_rec=np.zeros((D + 1, len(heads))))
     thr = [-1.0] if fixed else list(w.thresholds)
     dec_T = opts.get("decode_T", w.thresholds[0])
     for gi, hd in enumerate(heads):
@@ -82,11 +83,13 @@ def oracle_case(name):
         res["enc_out"].append(prof.out_last)
         prof.kept = kept
         st = O.compact_head(prof, hd["k"][:N_], hd["v"][:N_], member, N_, hd["slope"], hd["sink"])
+        res["dec_rec"][0, gi] = st.recovery
         for t in range(D):
             pos = N_ + t
             o = O.decode_head(st, hd["q"][pos], hd["k"][pos], hd["v"][pos], pos, hd["cls"], N_)
             res["dec_kept"][t, gi, st.positions] = True
             res["dec_out"][t, gi] = o
+            res["dec_rec"][t + 1, gi] = st.recovery
     for k in ("R", "cost", "choice", "colsum", "lastrow", "enc_kept", "enc_out", "dec_choice"):
         res[k] = np.asarray(res[k])
     return res

@@ -28,6 +28,12 @@ def test_oracle_matches_reference_golden(name):
     # decode: per-step kept sets bit-exact and outputs
     np.testing.assert_array_equal(o["dec_kept"], g["dec_kept"])
     np.testing.assert_allclose(o["dec_out"], g["dec_out"], rtol=1e-9, atol=1e-11)
+    # diagnostics: recovery of the attended set vs the uncompressed shadow
+    # softmax at every step, and the per-step mean over heads (StepRecord)
+    np.testing.assert_allclose(o["dec_rec"], g["dec_rec"], rtol=0, atol=1e-12)
+    rows = g["dec_mean"].shape[0]
+    np.testing.assert_allclose(o["dec_rec"].reshape(o["dec_rec"].shape[0], rows, -1).mean(-1).T,
+                               g["dec_mean"], rtol=0, atol=1e-12)
 
 
 def test_golden_cases_exercise_every_policy_kind():

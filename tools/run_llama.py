@@ -51,6 +51,8 @@ def main():
     ap.add_argument("--T", type=float, default=0.95)
     ap.add_argument("--mode", default="gather", choices=["gather", "tp", "dp"])
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--diagnostics", action="store_true",
+                    help="per-step recovery vs uncompressed attention (shadow keys)")
     args = ap.parse_args()
     cfg, B, N, D = PRESETS[args.config]
     if args.layers:
@@ -97,11 +99,12 @@ def main():
         torch.distributed.barrier()
     torch.cuda.synchronize()
     ev[0].record()
-    pre = model.prefill(tokens, pc, max_new_tokens=D)
+    pre = model.prefill(tokens, pc, max_new_tokens=D, diagnostics=args.diagnostics)
     ev[1].record()
     out = torch.empty(tokens.shape[0], D, dtype=torch.int64, device="cuda")
     for t in range(D):
         out[:, t] = model.decode_step()
+    mean_rec = model.mean_recovery() if args.diagnostics else None
     ev[2].record()
     torch.cuda.synchronize()
     model.check()
@@ -137,7 +140,7 @@ def main():
         cache_tokens=cache_tokens, full_cache_tokens=full_tokens,
         pruned_ratio=1 - cache_tokens / full_tokens, policies=pol,
         deterministic=deterministic, full_heads_exact=bool(full_ok), live_bounded=bool(bound_ok),
-        first_tokens=out[0, :8].tolist(),
+        first_tokens=out[0, :8].tolist(), mean_recovery_last_step=mean_rec,
         mem_gb=torch.cuda.max_memory_allocated() / 1e9)
     if rank == 0:
         print(json.dumps(line))
