@@ -109,6 +109,9 @@ typedef struct akv_profile_args {
   int32_t* topk_thr_pos_dev;     /*   position p is in the set iff (bits(colsum[p]), -p) >= (key, -pos) */
   void* workspace_dev;
   size_t workspace_bytes;
+  int32_t local_len;             /* prompt length anchoring the local budget (0 = N); re-profiling a
+                                    prompt plus generated tokens passes the true prompt length
+                                    (engine.py:161-176, metrics.py:140-187) */
 } akv_profile_args;
 
 size_t akv_profile_workspace_size(int32_t B, int32_t H, int32_t N, int32_t d);

@@ -40,6 +40,7 @@ class ProfileArgs(C.Structure):
         ("choice_dev", P), ("kept_pos_dev", P), ("kept_count_dev", P),
         ("last_row_recovery_dev", P), ("topk_gap_dev", P), ("topk_thr_key_dev", P),
         ("topk_thr_pos_dev", P), ("workspace_dev", P), ("workspace_bytes", sz),
+        ("local_len", i32),
     ]
 
 

@@ -271,6 +271,7 @@ struct PolicyParams {
   int n_thr;
   double thr[AKV_MAX_THRESHOLDS];
   int rows, criterion;
+  int local_len;  // prompt length anchoring the local budget (policies.py:209-211)
   float* out_last;
   double* recovery;
   int32_t* cost;
@@ -331,7 +332,7 @@ __global__ void __launch_bounds__(kPolicyThreads) k1_policy(PolicyParams p) {
     const int c = cls[j];
     bool k = ((at & AKV_ATOM_SPECIAL) && c == AKV_CLS_SPECIAL) ||
              ((at & AKV_ATOM_PUNCT) && c == AKV_CLS_PUNCT);
-    if (at & AKV_ATOM_LOCAL) k |= j >= N - budget(p.r_l[f], N);
+    if (at & AKV_ATOM_LOCAL) k |= j >= N - budget(p.r_l[f], p.local_len);
     if (at & AKV_ATOM_FREQUENT)
       k |= topk_selected(__double_as_longlong(colsum[j]), j, s_thr_key[f], s_thr_pos[f]);
     return k;
@@ -507,6 +508,9 @@ extern "C" int akv_profile(const akv_profile_args* a, void* stream) {
   pol.n_thr = a->n_thresholds;
   for (int t = 0; t < a->n_thresholds; ++t) pol.thr[t] = a->thresholds[t];
   pol.rows = a->rows; pol.criterion = a->criterion;
+  pol.local_len = a->local_len > 0 ? a->local_len : a->N;
+  if (pol.local_len > a->N)
+    return set_error(AKV_ERR_INVALID, "akv_profile: local_len %d exceeds N %d", a->local_len, a->N);
   pol.out_last = a->out_last_dev; pol.recovery = a->recovery_dev; pol.cost = a->cost_dev;
   pol.cosine = a->cosine_dev; pol.choice = a->choice_dev; pol.kept_pos = a->kept_pos_dev;
   pol.kept_count = a->kept_count_dev; pol.last_row_recovery = a->last_row_recovery_dev;

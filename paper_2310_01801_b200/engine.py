@@ -204,7 +204,7 @@ def _family_arrays(family, args):
 def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None = None,
                           fixed_policy: CompressionPolicy | None = None, *, prompt_len=None,
                           max_new_tokens: int = 0, extra_thresholds=(), slopes=None,
-                          sinks=None, diagnostics: bool = False):
+                          sinks=None, diagnostics: bool = False, local_len: int = 0):
     """Profile, select and compact every head of a batch (Alg. 1,
     engine.py:203-272) on the GPU.
 
@@ -299,6 +299,7 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
                                "cosine", "choice", "kept_pos", "kept_count", "lrr", "gap"))
     a.topk_thr_key_dev, a.topk_thr_pos_dev = _ptr(out["thr_key"]), _ptr(out["thr_pos"])
     a.workspace_dev, a.workspace_bytes = _ptr(ws), ws_bytes
+    a.local_len = int(local_len)
     stream = _stream()
     check(lib.akv_profile(C.byref(a), stream), ProfilerError)
 
@@ -515,6 +516,46 @@ def _model_rows(model, grid, positions, klass_of, prompt_len):
     return q, k, v
 
 
+def encode_model_rows(model, tokens, profiler_cfg: ProfilerConfig | None,
+                      fixed_policy: CompressionPolicy | None = None, *, prompt_len=None,
+                      max_new_tokens: int = 0, diagnostics: bool = False,
+                      extra_thresholds=()):
+    """The GPU counterpart of prompt_head_data + profiling (engine.py:161-200):
+    gather every head's rows for ``tokens`` from the duck-typed model (rows
+    anchored to ``prompt_len``, default len(tokens), which also anchors the
+    local budget), then profile (K1) and compact (K2).  Returns
+    (ProfileResult, CompressedCache, sorted grid, annotations)."""
+    tokens = list(tokens)
+    if not tokens:
+        raise EngineError("empty prompt")
+    n = len(tokens)
+    p = n if prompt_len is None else int(prompt_len)
+    if not 1 <= p <= n:
+        raise EngineError(f"prompt_len {p} out of range for {n} tokens")
+    grid = sorted(model.config.head_grid())
+    annotations = classify_tokens(tokens, model.vocab)
+    q, k, v = _model_rows(model, grid, range(n), lambda i: annotations[i].klass, p)
+    dev = torch.device("cuda")
+    cls = torch.tensor([[CLASS_CODE[a.klass] for a in annotations]], dtype=torch.uint8)
+    res, cache = encode_prompt_tensors(
+        torch.from_numpy(q).to(dev), torch.from_numpy(k).to(dev), torch.from_numpy(v).to(dev),
+        cls.to(dev), profiler_cfg, fixed_policy, max_new_tokens=max_new_tokens,
+        diagnostics=diagnostics, local_len=p if p != n else 0,
+        extra_thresholds=extra_thresholds)
+    return res, cache, grid, annotations
+
+
+def profile_of(res: ProfileResult, grid, t: int = 0) -> HeadProfile:
+    """HeadProfile (profiler.py:181-228) of threshold column ``t`` of a
+    ProfileResult whose heads are ``grid`` in order."""
+    decisions = {}
+    for gi, key in enumerate(grid):
+        c = int(res.choice[gi, t])
+        decisions[key] = HeadDecision(res.family[c], float(res.recovery[gi, c]),
+                                      int(res.cost[gi, c]))
+    return HeadProfile(decisions)
+
+
 def encode_prompt(model, prompt_tokens, profiler_cfg: ProfilerConfig | None,
                   fixed_policy: CompressionPolicy | None = None, threads=None,
                   diagnostics: bool = True, max_new_tokens: int = 256):
@@ -527,26 +568,11 @@ def encode_prompt(model, prompt_tokens, profiler_cfg: ProfilerConfig | None,
     """
     if profiler_cfg is None and fixed_policy is None:
         raise EngineError("need a profiler config or a fixed policy")
-    prompt_tokens = list(prompt_tokens)
-    if not prompt_tokens:
-        raise EngineError("empty prompt")
-    grid = sorted(model.config.head_grid())
-    n = len(prompt_tokens)
-    annotations = classify_tokens(prompt_tokens, model.vocab)
-    q, k, v = _model_rows(model, grid, range(n), lambda p: annotations[p].klass, n)
-    dev = torch.device("cuda")
-    cls = torch.tensor([[CLASS_CODE[a.klass] for a in annotations]], dtype=torch.uint8)
-    res, cache = encode_prompt_tensors(
-        torch.from_numpy(q).to(dev), torch.from_numpy(k).to(dev), torch.from_numpy(v).to(dev),
-        cls.to(dev), profiler_cfg, fixed_policy, max_new_tokens=max_new_tokens,
+    res, cache, grid, annotations = encode_model_rows(
+        model, prompt_tokens, profiler_cfg, fixed_policy, max_new_tokens=max_new_tokens,
         diagnostics=diagnostics)
-    choice = res.choice[:, 0]
-    decisions = {}
-    for gi, key in enumerate(grid):
-        pol = res.family[choice[gi]]
-        decisions[key] = HeadDecision(pol, float(res.recovery[gi, choice[gi]]),
-                                      int(res.cost[gi, choice[gi]]))
-    profile = HeadProfile(decisions)
+    dev = cache.device
+    profile = profile_of(res, grid)
     cache.profile = profile
     cache.keys = grid
     cache.annotations = list(annotations)

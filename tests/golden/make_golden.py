@@ -258,12 +258,63 @@ def make_mixed():
         dec_kept=np.packbits(dec_kept, axis=-1), dec_out=dec_out, dec_rec=dec_rec)
 
 
+def make_metrics():
+    """Reference metrics.py reports (tradeoff_curve, consistency_report,
+    compare_adaptive_vs_fixed, layer_distribution_report and their CSV /
+    JSON renderings) on the FoldedArrayModel of metrics_model.py."""
+    import json
+
+    import metrics_model as MM
+    from adaptive_kv import metrics as RM
+    from adaptive_kv.engine import GenerationConfig, generate
+
+    vocab = VocabMetadata(special_ids=frozenset(MM.SPECIAL), punctuation_ids=frozenset(MM.PUNCT))
+    model = MM.FoldedArrayModel(vocab, TokenClass.SPECIAL)
+    prompt = model.prompt_token_ids()
+    T_values = [0.5, 0.8, 0.9, 0.95, 0.98, 0.99, 0.995, 0.999, 1.0]
+    points = RM.tradeoff_curve(model, prompt, T_values)
+    cfg = ProfilerConfig(recovery_threshold=0.95)
+    entries = RM.consistency_report(model, prompt, [1, 4, 9, 17], cfg, max_new_tokens=24)
+    gen_cfg = GenerationConfig(max_new_tokens=12)
+    fixed = [parse_policy("special+punct+frequent(r_f=0.3)+local(r_l=0.3)"),
+             parse_policy("frequent(r_f=0.25)"), parse_policy("local(r_l=0.2)")]
+    extra = {"drop_punct": ProfilerConfig(recovery_threshold=0.95,
+                                          feasible=feasible_set(drop=[PolicyAtom.PUNCTUATION]))}
+    rows = RM.compare_adaptive_vs_fixed(model, prompt, cfg, fixed, gen_cfg, extra_adaptive=extra)
+    adaptive = generate(model, prompt, cfg, gen_cfg)
+    prof = adaptive.profile
+    dist = RM.layer_distribution_report(prof)
+    reports = {
+        "tradeoff": RM.tradeoff_rows(points), "consistency": RM.consistency_rows(entries),
+        "comparison": RM.comparison_rows(rows), "layers": RM.layer_distribution_rows(dist),
+    }
+    np.savez_compressed(
+        C.golden_path("metrics"),
+        T=np.array([p.T for p in points]), pruned=np.array([p.pruned_ratio for p in points]),
+        mean_rec=np.array([p.mean_recovery for p in points]),
+        cons_step=np.array([e.step for e in entries]),
+        cons_key=np.array([(e.layer, e.head) for e in entries]),
+        cons_policy=np.array([e.policy for e in entries]),
+        cons_match=np.array([e.matches_first for e in entries]),
+        cmp_method=np.array([r.method for r in rows]),
+        cmp_pruned=np.array([r.pruned_ratio for r in rows]),
+        cmp_rec=np.array([r.mean_step_recovery for r in rows]),
+        gen_tokens=np.array(adaptive.tokens), profile_csv=np.array(prof.to_csv()),
+        layers_json=np.array(json.dumps({str(k): v for k, v in dist.items()}, sort_keys=True)),
+        csv=np.array([RM.rows_to_csv(*reports[k]) for k in sorted(reports)]),
+        json=np.array([RM.rows_to_json(k, *reports[k]) for k in sorted(reports)]),
+        report_names=np.array(sorted(reports)),
+        stability=np.array(RM.stability_fraction(entries)))
+
+
 def main(argv):
-    names = argv or list(C.CASES) + [C.MIXED["name"]]
+    names = argv or list(C.CASES) + [C.MIXED["name"], "metrics"]
     for name in names:
         t0 = time.time()
         if name == C.MIXED["name"]:
             make_mixed()
+        elif name == "metrics":
+            make_metrics()
         else:
             make_workload_case(name)
         print(f"{name}: {time.time() - t0:.1f}s", flush=True)
