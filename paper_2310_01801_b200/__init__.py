@@ -23,5 +23,11 @@ from .profiler import (HeadDecision, HeadProfile, ProfilerConfig, ProfilerError,
                        profile_model, recovery_ratio, select_policy, select_policy_by_similarity,
                        tv_distance_row)
 from .tokens import TokenAnnotation, TokenClass, VocabMetadata, classify_tokens
+from .metrics import (MemoryModel, MetricsError, TradeoffPoint, compare_adaptive_vs_fixed,
+                      consistency_report, full_cache_bytes, layer_distribution_report,
+                      pruned_ratio, sidecar_overhead_fraction, tradeoff_curve)
+from .trace import (AttentionTrace, ModelConfig, ModelError, TraceBlock, TraceDimensionError,
+                    TraceError, TraceHeaderError, TraceModel, TraceTruncatedError, read_trace,
+                    replay_tensors, trace_tensors, write_trace, write_trace_ndjson)
 
 __version__ = "0.1.0"

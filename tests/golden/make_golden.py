@@ -17,6 +17,7 @@ workload's own token ids.  Outputs are written to ``tests/golden/*.npz``.
 
 from __future__ import annotations
 
+import json
 import math
 import os
 import sys
@@ -307,14 +308,56 @@ def make_metrics():
         stability=np.array(RM.stability_fraction(entries)))
 
 
+def make_trace():
+    """AKVT files written by the reference (binary + NDJSON) of a recorded
+    run of the reference's small_model fixture (pkg/tests/conftest.py:64-73,
+    the recording of test_trace.py:124-162), plus the reference's generate()
+    replayed from that trace: tokens, profile CSV, per-step retained counts
+    and mean recoveries."""
+    from adaptive_kv.engine import GenerationConfig, generate, reference_generate
+    from adaptive_kv.model import Archetype, HeadPlan
+    from adaptive_kv.tokens import TokenAnnotation
+    from adaptive_kv.trace import (AttentionTrace, TraceBlock, TraceModel, read_trace,
+                                   write_trace, write_trace_ndjson)
+
+    config = ModelConfig(num_layers=2, num_heads=2, head_dim=16, vocab_size=32, seed=7)
+    plan = {(0, 0): HeadPlan(Archetype.SPECIAL_DOMINANT), (0, 1): HeadPlan(Archetype.LOCAL_DOMINANT),
+            (1, 0): HeadPlan(Archetype.COLUMN_SPARSE), (1, 1): HeadPlan(Archetype.DIFFUSE)}
+    model = SyntheticModel(config, plan, dominance=0.97)
+    prompt_len, steps = 24, 8
+    prompt = model.prompt_token_ids(prompt_len)
+    ref = reference_generate(model, prompt, GenerationConfig(max_new_tokens=steps))
+    all_tokens = prompt + ref.tokens[: steps - 1]
+    ann = [TokenAnnotation(p, t, model.vocab.classify_id(t)) for p, t in enumerate(all_tokens)]
+    blocks = {key: [TraceBlock(step=p, k=model.k_row(*key, p, ann[p].klass, prompt_len),
+                               v=model.v_row(*key, p), q=model.q_row(*key, p, prompt_len))
+                    for p in range(len(all_tokens))] for key in config.head_grid()}
+    trace = AttentionTrace(config, ann, blocks)
+    write_trace(trace, os.path.join(C.HERE, "replay.akvt"))
+    write_trace_ndjson(trace, os.path.join(C.HERE, "replay.ndjson"))
+    replay = TraceModel(read_trace(os.path.join(C.HERE, "replay.akvt")))
+    res = generate(replay, prompt, ProfilerConfig(recovery_threshold=0.95),
+                   GenerationConfig(max_new_tokens=steps))
+    grid = config.head_grid()
+    np.savez_compressed(
+        C.golden_path("replay"), prompt_len=prompt_len, steps=steps,
+        tokens=np.array(res.tokens), profile_csv=np.array(res.profile.to_csv()),
+        retained=np.array([[r.head_retained[k] for k in grid] for r in res.records]),
+        mean_rec=np.array([r.mean_recovery for r in res.records]),
+        retained_pos=np.array([json.dumps({f"{k[0]},{k[1]}": list(r.retained_positions[k])
+                                           for k in grid}) for r in res.records]))
+
+
 def main(argv):
-    names = argv or list(C.CASES) + [C.MIXED["name"], "metrics"]
+    names = argv or list(C.CASES) + [C.MIXED["name"], "metrics", "replay"]
     for name in names:
         t0 = time.time()
         if name == C.MIXED["name"]:
             make_mixed()
         elif name == "metrics":
             make_metrics()
+        elif name == "replay":
+            make_trace()
         else:
             make_workload_case(name)
         print(f"{name}: {time.time() - t0:.1f}s", flush=True)
