@@ -127,8 +127,8 @@ template <typename T>
 __global__ void __launch_bounds__(128) k_rope_scatter(akv_rope_args a) {
   const int half = a.d / 2;
   const int hpb = 128 / half;
-  const int t = blockIdx.y;
-  const int h = blockIdx.x * hpb + threadIdx.x / half;
+  const int t = blockIdx.x;  // tokens on x: up to 2^31-1 (y is capped at 65535)
+  const int h = blockIdx.y * hpb + threadIdx.x / half;
   const int c = threadIdx.x % half;
   if (h >= a.Hl) return;
   const int b = t / a.n, i = t % a.n;
@@ -294,7 +294,7 @@ extern "C" int akv_rope_scatter(const akv_rope_args* a, void* stream) {
   if (a->T % a->n || a->row0 + a->n > a->out_ld)
     return set_error(AKV_ERR_INVALID, "akv_rope_scatter: T %% n != 0 or rows exceed out_ld");
   const int hpb = 128 / (a->d / 2);
-  dim3 grid((a->Hl + hpb - 1) / hpb, a->T);
+  dim3 grid(a->T, (a->Hl + hpb - 1) / hpb);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (a->dtype == AKV_DTYPE_F32)
     k_rope_scatter<float><<<grid, 128, 0, st>>>(*a);

@@ -80,6 +80,10 @@ class ShardPlan:
     rank: int = 0
     world: int = 1
     mode: str = "gather"
+    # False: this process computes rank `rank`'s shard but issues no
+    # collective (single-GPU measurement of one rank's compute; the outputs
+    # are then not those of the full model)
+    comm: bool = True
 
     def heads(self, H: int) -> tuple:
         if H % self.world:
@@ -243,10 +247,15 @@ class FastGenLlama:
         blocks = global head order)."""
         if self.plan.mode == "tp":
             return o
+        if not self.plan.comm:   # compute-only shard: the local block in place, zeros elsewhere
+            full = torch.zeros(o.shape[0], self.plan.world * o.shape[1], dtype=o.dtype,
+                               device=o.device)
+            full[:, self.plan.rank * o.shape[1]:(self.plan.rank + 1) * o.shape[1]] = o
+            return full
         return gather_head_blocks(o, self.plan.world, self.group)
 
     def _reduce(self, x):
-        if self.plan.mode != "tp":
+        if self.plan.mode != "tp" or not self.plan.comm:
             return x
         return all_reduce_partial(x, self.plan.world, self.group)
 

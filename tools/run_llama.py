@@ -51,6 +51,9 @@ def main():
     ap.add_argument("--T", type=float, default=0.95)
     ap.add_argument("--mode", default="gather", choices=["gather", "tp", "dp"])
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--simulate-world", type=int, default=0,
+                    help="one process computes rank 0's shard of a P-way split without "
+                         "collectives (per-GPU compute of a multi-GPU config on one GPU)")
     ap.add_argument("--diagnostics", action="store_true",
                     help="per-step recovery vs uncompressed attention (shadow keys)")
     args = ap.parse_args()
@@ -72,6 +75,10 @@ def main():
         per = B // world
         ids = ids[rank * per:(rank + 1) * per]
         plan = ShardPlan()
+    elif args.simulate_world > 1:
+        if world > 1:
+            raise SystemExit("--simulate-world is a single-process measurement")
+        plan = ShardPlan(0, args.simulate_world, args.mode, comm=False)
     else:
         plan = ShardPlan(rank, world, args.mode)
     t0 = time.time()
@@ -134,6 +141,8 @@ def main():
     line = dict(
         config=args.config, n_layers=cfg.n_layers, batch=B, prompt=N, decode=D, T=args.T,
         mode=args.mode, world=world, rank=rank, init_s=round(init_s, 1),
+        simulated_world=args.simulate_world or None,
+        local_heads=model.Hl, local_ffn=model.Fl,
         prefill_ms=prefill_ms, profiling_ms_per_layer=float(np.mean(prof_ms)),
         profiling_ms_total=float(np.sum(prof_ms)),
         decode_ms=decode_ms, decode_ms_per_step=decode_ms / D, decode_tok_s=dec_tok_s,
