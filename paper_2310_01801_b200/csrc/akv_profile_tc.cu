@@ -73,6 +73,42 @@ __device__ __forceinline__ void mma_tile(uint32_t tmem_d, const uint8_t* a_tile,
   }
 }
 
+// online (max, sum) update of a row with 64 logits already in the log2
+// domain (masked entries -inf)
+__device__ __forceinline__ void row_update_scaled(const float* v, float& m, float& l) {
+  float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+  for (int c = 0; c < 64; ++c) mx[c & 3] = fmaxf(mx[c & 3], v[c]);
+  const float mn = fmaxf(fmaxf(m, fmaxf(mx[0], mx[1])), fmaxf(mx[2], mx[3]));
+  if (mn == -INFINITY) return;
+  float sm[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int c = 0; c < 64; ++c) {
+    const float x = v[c] - mn;
+    sm[c & 3] += exp2_mixed(x, c);
+  }
+  l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + ((sm[0] + sm[1]) + (sm[2] + sm[3]));
+  m = mn;
+}
+
+// the same on raw accumulator values: the max is taken before scaling
+// (scale > 0) and the scale folds into one FFMA per exponential
+__device__ __forceinline__ void row_update_raw(const float* v, float sl2, float& m, float& l) {
+  float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+  for (int c = 0; c < 64; ++c) mx[c & 3] = fmaxf(mx[c & 3], v[c]);
+  const float mn = fmaxf(m, fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * sl2);
+  const float nb = -mn;
+  float sm[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int c = 0; c < 64; ++c) {
+    const float x = fmaf(v[c], sl2, nb);
+    sm[c & 3] += exp2_mixed(x, c);
+  }
+  l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + ((sm[0] + sm[1]) + (sm[2] + sm[3]));
+  m = mn;
+}
+
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kTcThreads, 2)
     k1tc_rowlse(const __grid_constant__ TcParams p, const __grid_constant__ CUtensorMap tmQ,
@@ -83,7 +119,7 @@ __global__ void __launch_bounds__(kTcThreads, 2)
   uint8_t* sK = smem + kTileB;
   __shared__ __align__(8) uint64_t q_full, k_full[kRing], k_empty[kRing], acc_full[2], acc_empty[2];
   __shared__ uint32_t s_tmem;
-  __shared__ float s_col[2][kTT];
+  __shared__ __align__(16) float s_col[2][kTT];
   const int ntiles = (p.N + kTT - 1) / kTT;
   const int g = blockIdx.y, h = g % p.H, b = g / p.H;
   const int qt = ntiles - 1 - blockIdx.x;  // heaviest (most key tiles) first
@@ -144,7 +180,8 @@ __global__ void __launch_bounds__(kTcThreads, 2)
     const float sink_l2 = (p.sink ? p.sink[h] : 0.f) * kLog2e;
     const bool bias = slope_l2 != 0.f || sink_l2 != 0.f;
     const uint8_t* cls = p.cls + (size_t)b * p.cls_ld;
-    const float rowterm = -slope_l2 * (float)row;
+    // logits in the log2 domain without the row term -slope*row, which is
+    // constant along a row and joins the lse at the end
     float m = -INFINITY, l = 0.f;
     uint8_t cnext = 0;
     if (bias && et < kTT) cnext = et < p.N ? cls[et] : 0;
@@ -161,35 +198,36 @@ __global__ void __launch_bounds__(kTcThreads, 2)
       }
       mbar_wait(&acc_full[a], (kt >> 1) & 1);
       tc_fence_after();
-      const bool masked = (kt == qt) || ((kt + 1) * kTT > p.N);
-#pragma unroll 1
-      for (int ch = 2 * half; ch < 2 * half + 2; ++ch) {
-        float v[32];
-        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + a * kTT + ch * 32, v);
-        float cm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          float x = v[c] * sl2;
-          if (bias) x += s_col[a][ch * 32 + c] + rowterm;
-          if (masked) {
-            const int col = kt * kTT + ch * 32 + c;
-            if (col > row || col >= p.N) x = -INFINITY;
-          }
-          v[c] = x;
-          cm[c & 3] = fmaxf(cm[c & 3], x);
-        }
-        const float mn = fmaxf(m, fmaxf(fmaxf(cm[0], cm[1]), fmaxf(cm[2], cm[3])));
-        if (mn != -INFINITY) {
-          float sm[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-          for (int c = 0; c < 32; ++c) sm[c & 3] += fast_exp2(v[c] - mn);
-          l = (m == -INFINITY ? 0.f : l * fast_exp2(m - mn)) + ((sm[0] + sm[1]) + (sm[2] + sm[3]));
-          m = mn;
-        }
-      }
+      float v[64];
+      tmem_ld64(tmem + ((uint32_t)(quarter * 32) << 16) + a * kTT + half * 64, v);
+      // the values are in registers: hand the accumulator back to the MMA warp
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[a]);
+      const bool masked = (kt == qt) || ((kt + 1) * kTT > p.N);
+      const float* ct = &s_col[a][half * 64];
+      if (masked) {  // diagonal / ragged tile: causal and length masks
+        const int c0 = kt * kTT + half * 64;
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          float y = bias ? fmaf(v[c], sl2, ct[c]) : v[c] * sl2;
+          if (c0 + c > row || c0 + c >= p.N) y = -INFINITY;
+          v[c] = y;
+        }
+        row_update_scaled(v, m, l);
+      } else if (bias) {
+#pragma unroll
+        for (int c = 0; c < 64; c += 4) {
+          const float4 t = *reinterpret_cast<const float4*>(ct + c);
+          v[c] = fmaf(v[c], sl2, t.x);
+          v[c + 1] = fmaf(v[c + 1], sl2, t.y);
+          v[c + 2] = fmaf(v[c + 2], sl2, t.z);
+          v[c + 3] = fmaf(v[c + 3], sl2, t.w);
+        }
+        row_update_scaled(v, m, l);
+      } else {
+        row_update_raw(v, sl2, m, l);
+      }
     }
     // merge the two column halves of every row
     if (half == 1) { s_ml[rl][0] = m; s_ml[rl][1] = l; }
@@ -199,7 +237,8 @@ __global__ void __launch_bounds__(kTcThreads, 2)
       const float mm = fmaxf(m, m2);
       const float ll = (m == -INFINITY ? 0.f : l * fast_exp2(m - mm)) +
                        (m2 == -INFINITY ? 0.f : l2 * fast_exp2(m2 - mm));
-      if (row < p.N) p.lse[(size_t)g * p.N + row] = (mm + __log2f(ll)) * kLn2;
+      const float rowterm = -slope_l2 * (float)row;
+      if (row < p.N) p.lse[(size_t)g * p.N + row] = (mm + rowterm + __log2f(ll)) * kLn2;
     }
   }
   tc_fence_before();
@@ -220,7 +259,7 @@ __global__ void __launch_bounds__(kTcThreads, 2)
   uint8_t* sQ = smem + kTileB;
   __shared__ __align__(8) uint64_t k_full, q_full[kRing], q_empty[kRing], acc_full[2], acc_empty[2];
   __shared__ uint32_t s_tmem;
-  __shared__ float s_col[2][kTT];
+  __shared__ __align__(16) float s_col[2][kTT];
   __shared__ float s_lastp[kTT];
   const int ntiles = (p.N + kTT - 1) / kTT;
   const int g = blockIdx.y, h = g % p.H, b = g / p.H;
@@ -283,9 +322,13 @@ __global__ void __launch_bounds__(kTcThreads, 2)
     const float sink_l2 = (p.sink ? p.sink[h] : 0.f) * kLog2e;
     const uint8_t* cls = p.cls + (size_t)b * p.cls_ld;
     const float* lse = p.lse + (size_t)g * p.N;
-    // per-key term: sink on a special key, + slope * key
-    const float kterm = (key < p.N && cls[key] == AKV_CLS_SPECIAL ? sink_l2 : 0.f) +
-                        slope_l2 * (float)key;
+    // per-key term: sink on a special key, + slope * key.  Without a slope
+    // the key term is a constant factor of the key's column and is applied
+    // to the tile sums (kfac) instead of inside every exponential.
+    const float ksink = key < p.N && cls[key] == AKV_CLS_SPECIAL ? sink_l2 : 0.f;
+    const bool slope_on = slope_l2 != 0.f;
+    const float kterm = ksink + slope_l2 * (float)key;
+    const float kfac = fast_exp2(ksink);
     double dsum = 0.0, dsq = 0.0;
     float lastp = 0.f;
     const int qlast = p.N - 1;
@@ -303,30 +346,61 @@ __global__ void __launch_bounds__(kTcThreads, 2)
       EpiSync::sync();
       mbar_wait(&acc_full[a], (i >> 1) & 1);
       tc_fence_after();
-      // diagonal tile (causal mask), ragged tail (q >= N) and the tile holding row N-1
-      const bool masked = (i == 0) || ((qt + 1) * kTT > p.N) || (qt == qlast / kTT);
-      float ts[4] = {0.f, 0.f, 0.f, 0.f}, tq[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
-      for (int ch = 2 * half; ch < 2 * half + 2; ++ch) {
-        float v[32];
-        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + a * kTT + ch * 32, v);
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          float pr = fast_exp2(fmaf(v[c], sl2, kterm + s_col[a][ch * 32 + c]));
-          if (masked) {
-            const int q = qt * kTT + ch * 32 + c;
-            if (q < key || q >= p.N) pr = 0.f;
-            if (q == qlast) lastp = pr;
-          }
-          ts[c & 3] += pr;
-          tq[c & 3] = fmaf(pr, pr, tq[c & 3]);
-        }
-      }
-      dsum += (double)((ts[0] + ts[1]) + (ts[2] + ts[3]));
-      dsq += (double)((tq[0] + tq[1]) + (tq[2] + tq[3]));
+      float v[64];
+      tmem_ld64(tmem + ((uint32_t)(quarter * 32) << 16) + a * kTT + half * 64, v);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[a]);
+      // diagonal tile (causal mask), ragged tail (q >= N) and the tile holding row N-1
+      const bool masked = (i == 0) || ((qt + 1) * kTT > p.N) || (qt == qlast / kTT);
+      const float* ct = &s_col[a][half * 64];
+      float ts[4] = {0.f, 0.f, 0.f, 0.f}, tq[4] = {0.f, 0.f, 0.f, 0.f};
+      if (masked) {
+        const int q0 = qt * kTT + half * 64;
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          float pr = fast_exp2(fmaf(v[c], sl2, kterm + ct[c]));
+          const int q = q0 + c;
+          if (q < key || q >= p.N) pr = 0.f;
+          if (q == qlast) lastp = pr;
+          ts[c & 3] += pr;
+          tq[c & 3] = fmaf(pr, pr, tq[c & 3]);
+        }
+        dsum += (double)((ts[0] + ts[1]) + (ts[2] + ts[3]));
+        dsq += (double)((tq[0] + tq[1]) + (tq[2] + tq[3]));
+      } else if (slope_on) {
+#pragma unroll
+        for (int c = 0; c < 64; c += 4) {
+          const float4 t = *reinterpret_cast<const float4*>(ct + c);
+          const float tt[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float x = fmaf(v[c + u], sl2, kterm + tt[u]);
+            const float pr = exp2_mixed(x, u);
+            ts[u] += pr;
+            tq[u] = fmaf(pr, pr, tq[u]);
+          }
+        }
+        dsum += (double)((ts[0] + ts[1]) + (ts[2] + ts[3]));
+        dsq += (double)((tq[0] + tq[1]) + (tq[2] + tq[3]));
+      } else {
+#pragma unroll
+        for (int c = 0; c < 64; c += 4) {
+          const float4 t = *reinterpret_cast<const float4*>(ct + c);
+          const float tt[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float x = fmaf(v[c + u], sl2, tt[u]);
+            const float pr = exp2_mixed(x, u);
+            ts[u] += pr;
+            tq[u] = fmaf(pr, pr, tq[u]);
+          }
+        }
+        const float s1 = (ts[0] + ts[1]) + (ts[2] + ts[3]);
+        const float s2 = (tq[0] + tq[1]) + (tq[2] + tq[3]);
+        dsum += (double)(s1 * kfac);
+        dsq += (double)(s2 * (kfac * kfac));
+      }
     }
     // the last query row lies in the last (masked) tile; merge the halves
     if (half == 1) { s_part[0][kl] = dsum; s_part[1][kl] = dsq; s_plast[kl] = lastp; }

@@ -75,10 +75,63 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 64 consecutive fp32 columns of this thread's TMEM lane: two x32 loads in
+// flight behind one wait
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float* v) {
+  uint32_t r[64];
+#define AKV_LD32(OFF, R)                                                                        \
+  asm volatile(                                                                                 \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"        \
+      : "=r"(R[0]), "=r"(R[1]), "=r"(R[2]), "=r"(R[3]), "=r"(R[4]), "=r"(R[5]), "=r"(R[6]),   \
+        "=r"(R[7]), "=r"(R[8]), "=r"(R[9]), "=r"(R[10]), "=r"(R[11]), "=r"(R[12]),             \
+        "=r"(R[13]), "=r"(R[14]), "=r"(R[15]), "=r"(R[16]), "=r"(R[17]), "=r"(R[18]),          \
+        "=r"(R[19]), "=r"(R[20]), "=r"(R[21]), "=r"(R[22]), "=r"(R[23]), "=r"(R[24]),          \
+        "=r"(R[25]), "=r"(R[26]), "=r"(R[27]), "=r"(R[28]), "=r"(R[29]), "=r"(R[30]),          \
+        "=r"(R[31])                                                                             \
+      : "r"(taddr + (OFF)))
+  AKV_LD32(0, r);
+  AKV_LD32(32, (r + 32));
+#undef AKV_LD32
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x for x <= 0 on the FMA pipe (MUFU stays free for the other lanes of the
+// work): x = j + f with j = round(x) taken from the mantissa of x + 1.5*2^23,
+// 2^f on [-0.5, 0.5] by a degree-5 minimax polynomial (max relative error
+// 1.9e-7 in fp32, like ex2.approx), 2^j added to the exponent field.  Inputs
+// below -125 clamp (the result is < 2^-125, negligible next to any sum of
+// probabilities); the caller guarantees x <= 0 (x - running max).
+__device__ __forceinline__ float exp2_fma(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  float p = 1.3264727e-3f;
+  p = fmaf(p, f, 9.6715129e-3f);
+  p = fmaf(p, f, 5.5507337e-2f);
+  p = fmaf(p, f, 2.4022242e-1f);
+  p = fmaf(p, f, 6.9314698e-1f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
+
+// share of the exponentials of the unmasked K1 tiles evaluated on the FMA
+// pipe: every kPolyEvery-th, 0 = none.  Measured on B200 at config 4: a
+// quarter on the FMA pipe left both passes unchanged (5.71 -> 5.73 ms and
+// 6.53 -> 6.83 ms): the epilogue is issue-bound, not MUFU-bound, so it is off.
+constexpr int kPolyEvery = 0;
+
+__device__ __forceinline__ float exp2_mixed(float x, int c) {
+  return (kPolyEvery > 0 && c % (kPolyEvery > 0 ? kPolyEvery : 1) == kPolyEvery - 1)
+             ? exp2_fma(x) : fast_exp2(x);
 }
 
 }  // namespace akv
