@@ -204,7 +204,8 @@ def _family_arrays(family, args):
 def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None = None,
                           fixed_policy: CompressionPolicy | None = None, *, prompt_len=None,
                           max_new_tokens: int = 0, extra_thresholds=(), slopes=None,
-                          sinks=None, diagnostics: bool = False, local_len: int = 0):
+                          sinks=None, diagnostics: bool = False, local_len: int = 0,
+                          k1_events=None):
     """Profile, select and compact every head of a batch (Alg. 1,
     engine.py:203-272) on the GPU.
 
@@ -301,7 +302,11 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
     a.workspace_dev, a.workspace_bytes = _ptr(ws), ws_bytes
     a.local_len = int(local_len)
     stream = _stream()
+    if k1_events is not None:   # (start, end) CUDA events around akv_profile (bench.py)
+        k1_events[0].record()
     check(lib.akv_profile(C.byref(a), stream), ProfilerError)
+    if k1_events is not None:
+        k1_events[1].record()
 
     # ragged arena plan (device prefix sum); the single device->host read of
     # the session sizes the arena and brings the profile summary along
