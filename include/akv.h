@@ -196,6 +196,8 @@ typedef struct akv_decode_args {
                                     replaces pos (so a captured CUDA graph can be replayed for
                                     successive steps) */
   int32_t flags;                 /* AKV_DECODE_* */
+  float* lse_out_dev;            /* optional [B*H] natural-log log-sum-exp of each head's attended
+                                    logits (live slots + the new token), for diagnostics */
 } akv_decode_args;
 
 /* akv_decode_args.flags: the previous kernel on the stream is this cache's
@@ -214,9 +216,11 @@ int akv_decode_workspace_init(void* workspace_dev, size_t workspace_bytes, int32
 
 /* ---- diagnostics: per-step recovery against uncompressed attention -----
  * Replaces engine.py:341-349 (shadow keys, full softmax of the new query,
- * recovery = mass on the attended positions).  Launch BEFORE the decode step
- * of the same position (live_in is the pre-eviction live set); it appends
- * the new key to the shadow rows and the new class to cls_hist. */
+ * recovery = mass on the attended positions).  Launch BEFORE
+ * akv_decode_step of the same position (live_in is the pre-eviction live set
+ * whose positions plus the new one are "attended"); it appends the new key
+ * to the position-indexed shadow rows (and the class to cls_hist), streams
+ * every shadow key once and writes the per-head recovery. */
 typedef struct akv_diag_args {
   int32_t B, H, d, dtype;
   int32_t pos;                   /* position of the new token (ignored when pos_dev is set) */
@@ -235,7 +239,12 @@ typedef struct akv_diag_args {
   uint8_t* cls_hist_dev;         /* [B, cls_ld] class of every position (in/out), or NULL */
   int64_t cls_ld;
   double* recovery_dev;          /* [B*H] out */
+  void* workspace_dev;           /* akv_decode_recovery_workspace_size bytes, initialised once */
+  size_t workspace_bytes;
 } akv_diag_args;
+size_t akv_decode_recovery_workspace_size(int32_t B, int32_t H, int64_t shadow_ld);
+int akv_decode_recovery_workspace_init(void* workspace_dev, size_t workspace_bytes, int32_t B,
+                                       int32_t H, int64_t shadow_ld, void* stream);
 int akv_decode_recovery(const akv_diag_args* a, void* stream);
 
 /* ---- reference single-context operations (float64, batched) ----------

@@ -66,7 +66,7 @@ class DecodeArgs(C.Structure):
         ("vc_dev", P), ("meta_dev", P), ("score_dev", P), ("base_live_dev", P), ("live_in_dev", P),
         ("live_out_dev", P), ("out_dev", P), ("evicted_dev", P), ("status_dev", P),
         ("max_cap", i32), ("total_slots", i64), ("workspace_dev", P), ("workspace_bytes", sz),
-        ("pos_dev", P), ("flags", i32),
+        ("pos_dev", P), ("flags", i32), ("lse_out_dev", P),
     ]
 
 
@@ -93,7 +93,7 @@ class DiagArgs(C.Structure):
         ("q_dev", P), ("k_dev", P), ("bh_stride", i64), ("new_cls_dev", P), ("slope_dev", P),
         ("sink_dev", P), ("seg_off_dev", P), ("live_in_dev", P), ("meta_dev", P),
         ("shadow_dev", P), ("shadow_ld", i64), ("cls_hist_dev", P), ("cls_ld", i64),
-        ("recovery_dev", P),
+        ("recovery_dev", P), ("workspace_dev", P), ("workspace_bytes", sz),
     ]
 
 
@@ -101,7 +101,8 @@ class DiagArgs(C.Structure):
 EXPORTS = (
     "akv_profile_workspace_size", "akv_profile", "akv_compact", "akv_plan_segments",
     "akv_decode_workspace_size", "akv_decode_step", "akv_decode_workspace_init",
-    "akv_decode_recovery",
+    "akv_decode_recovery", "akv_decode_recovery_workspace_size",
+    "akv_decode_recovery_workspace_init",
     "akv_softmax_rows_f64", "akv_causal_attention_f64", "akv_keep_mask", "akv_map_recovery_f64",
     "akv_update_scores_f64", "akv_gather_rows_f64", "akv_tv_distance_f64",
     "akv_embed_classify", "akv_add_rmsnorm", "akv_rope_scatter", "akv_swiglu",
@@ -138,6 +139,10 @@ def _load():
     lib.akv_tv_distance_f64.argtypes = [i32, P, P, P, P]
     lib.akv_decode_recovery.argtypes = [C.POINTER(DiagArgs), P]
     lib.akv_decode_recovery.restype = C.c_int
+    lib.akv_decode_recovery_workspace_size.argtypes = [i32, i32, i64]
+    lib.akv_decode_recovery_workspace_size.restype = sz
+    lib.akv_decode_recovery_workspace_init.argtypes = [P, sz, i32, i32, i64, P]
+    lib.akv_decode_recovery_workspace_init.restype = C.c_int
     lib.akv_embed_classify.argtypes = [i32, P, i32, P, P, i32, i32, P, P, P]
     lib.akv_add_rmsnorm.argtypes = [i32, i32, i32, P, P, P, C.c_float, P, P]
     lib.akv_rope_scatter.argtypes = [C.POINTER(RopeArgs), P]

@@ -89,6 +89,7 @@ struct DecParams {
   unsigned long long* trace;  // optional [grid, 8] globaltimer stamps (AKV_DEC_TRACE)
   const int32_t* pos_dev;     // device position (CUDA-graph replays), overrides pos
   int flags;                  // AKV_DECODE_* flags
+  float* lse_out;             // [G] log-sum-exp of each head's attended logits, or NULL
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -600,6 +601,7 @@ __device__ void head_epilogue(const DecParams& p, const HeadCtx& hc, int nparts,
       const int t = tid + u * NC;
       if (t < D) p.out[(size_t)g * D + t] = acc[u] * inv;
     }
+    if (p.lse_out && tid == 0) p.lse_out[g] = gM + logf(gl);
   }
   if (hc.atoms & AKV_ATOM_FULL) {  // the full cache never evicts
     if (tid == 0) {
@@ -1386,7 +1388,8 @@ extern "C" int akv_decode_step(const akv_decode_args* a, void* stream) {
               a->meta_dev, a->score_dev, a->base_live_dev, a->live_in_dev, a->live_out_dev,
               a->out_dev,
               a->evicted_dev, a->status_dev ? a->status_dev : w.status, w.part, w.logit, w.counter,
-              w.max_parts, (float)(1.0 / sqrt((double)a->d)), g_dec_trace, a->pos_dev, a->flags};
+              w.max_parts, (float)(1.0 / sqrt((double)a->d)), g_dec_trace, a->pos_dev, a->flags,
+              a->lse_out_dev};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaErrorInvalidValue;
   bool ok = true;

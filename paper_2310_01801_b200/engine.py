@@ -383,18 +383,25 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
         cache.cls_hist = torch.zeros(B, N + int(max_new_tokens), dtype=torch.uint8, device=dev)
         cache.cls_hist[:, :N].copy_(classes[:, :N])
         cache.step_recovery = cache.step_recovery.clone()
+        shadow_ld = cache.shadow.shape[1]
+        ws = lib.akv_decode_recovery_workspace_size(B, H, shadow_ld)
+        cache.diag_ws = torch.empty(ws, dtype=torch.uint8, device=dev)
+        check(lib.akv_decode_recovery_workspace_init(_ptr(cache.diag_ws), ws, B, H, shadow_ld,
+                                                     stream))
         g = _lib.DiagArgs()
         g.B, g.H, g.d, g.dtype = B, H, d, dt
         g.slope_dev, g.sink_dev = _ptr(slopes), _ptr(sinks)
         g.seg_off_dev, g.meta_dev = _ptr(cache.seg_off), _ptr(cache.meta)
-        g.shadow_dev, g.shadow_ld = _ptr(cache.shadow), cache.shadow.shape[1]
+        g.shadow_dev, g.shadow_ld = _ptr(cache.shadow), shadow_ld
         g.cls_hist_dev, g.cls_ld = _ptr(cache.cls_hist), cache.cls_hist.shape[1]
         g.recovery_dev = _ptr(cache.step_recovery)
+        g.workspace_dev, g.workspace_bytes = _ptr(cache.diag_ws), ws
         cache._diag_args = g
     return res, cache
 
 
 def _launch_recovery(cache, q, k, new_classes, live_in, pos=None, pos_dev=None):
+    """Before the decode step of the same position (pre-eviction live set)."""
     g = cache._diag_args
     g.pos = 0 if pos is None else pos
     g.pos_dev = _ptr(pos_dev)
