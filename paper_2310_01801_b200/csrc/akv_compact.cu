@@ -88,17 +88,26 @@ __global__ void __launch_bounds__(128) k2_compact(CompactParams p) {
   }
 }
 
-__global__ void k2_plan(int G, const int32_t* kept, int32_t extra, int32_t* cap, int64_t* off,
-                        int64_t* total) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  int64_t acc = 0;
-  for (int g = 0; g < G; ++g) {
-    const int c = ((kept[g] + extra + 7) / 8) * 8;  // 8-slot aligned segments
+constexpr int kPlanThreads = 1024;
+
+// one CTA: each thread owns a contiguous run of heads; block scan of the
+// run totals (8-slot aligned segments)
+__global__ void __launch_bounds__(kPlanThreads) k2_plan(int G, const int32_t* kept, int32_t extra,
+                                                        int32_t* cap, int64_t* off, int64_t* total) {
+  __shared__ int red[kPlanThreads / 32 + 1];
+  const int per = (G + blockDim.x - 1) / blockDim.x;
+  const int lo = min(G, (int)threadIdx.x * per), hi = min(G, lo + per);
+  int mine = 0;
+  for (int g = lo; g < hi; ++g) mine += ((kept[g] + extra + 7) / 8) * 8;
+  int tot;
+  int acc = block_exclusive_scan(mine, red, &tot);
+  for (int g = lo; g < hi; ++g) {
+    const int c = ((kept[g] + extra + 7) / 8) * 8;
     cap[g] = c;
     off[g] = acc;
     acc += c;
   }
-  *total = acc;
+  if (threadIdx.x == 0) *total = tot;
 }
 
 }  // namespace akv
@@ -109,8 +118,9 @@ extern "C" int akv_plan_segments(int32_t G, const int32_t* kept_count_dev, int32
                                  int32_t* seg_cap_dev, int64_t* seg_off_dev, int64_t* total_dev,
                                  void* stream) {
   if (G < 1 || extra < 0) return set_error(AKV_ERR_INVALID, "akv_plan_segments: bad G/extra");
-  k2_plan<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(G, kept_count_dev, extra, seg_cap_dev,
-                                                          seg_off_dev, total_dev);
+  k2_plan<<<1, kPlanThreads, 0, static_cast<cudaStream_t>(stream)>>>(G, kept_count_dev, extra,
+                                                                    seg_cap_dev, seg_off_dev,
+                                                                    total_dev);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(AKV_ERR_CUDA, "akv_plan_segments: %s", cudaGetErrorString(e));
   return AKV_OK;

@@ -308,20 +308,43 @@ __global__ void __launch_bounds__(kPolicyThreads) k1_policy(PolicyParams p) {
   };
   // exact frequent top-k thresholds (one per member with FREQUENT), and the
   // min relative gap at each boundary (k-th vs (k+1)-th largest score)
+  // One radix select per distinct frequent budget (members sharing r_f share
+  // the threshold); the (k+1)-th largest key for the gap is the largest key
+  // outside the selected set - a block max, not a second select.
+  __shared__ unsigned long long s_next[kPolicyThreads / 32];
   double min_gap = INFINITY;
+  int have = -1;  // a member whose threshold is already in s_thr_*
   for (int f = 0; f < p.n_family; ++f) {
     if (!(p.atoms[f] & AKV_ATOM_FREQUENT) || (p.atoms[f] & AKV_ATOM_FULL)) continue;
+    if (have >= 0 && p.r_f[have] == p.r_f[f]) {
+      if (threadIdx.x == 0) { s_thr_key[f] = s_thr_key[have]; s_thr_pos[f] = s_thr_pos[have]; }
+      __syncthreads();
+      continue;
+    }
     const int kb = budget(p.r_f[f], N);
     unsigned long long tk; int tp;
     block_topk_threshold(N, kb, get, hist, red_i, &tk, &tp);
     if (threadIdx.x == 0) { s_thr_key[f] = tk; s_thr_pos[f] = tp; }
     if (kb < N) {
-      unsigned long long tk2; int tp2;
-      block_topk_threshold(N, kb + 1, get, hist, red_i, &tk2, &tp2);
-      const double a = __longlong_as_double(tk), c = __longlong_as_double(tk2);
+      unsigned long long nk = 0ull;
+      for (int j = threadIdx.x; j < N; j += blockDim.x) {
+        const unsigned long long key = __double_as_longlong(colsum[j]);
+        if (!topk_selected(key, j, tk, tp) && key > nk) nk = key;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(0xffffffffu, nk, o);
+        nk = other > nk ? other : nk;
+      }
+      if ((threadIdx.x & 31) == 0) s_next[threadIdx.x >> 5] = nk;
+      __syncthreads();
+      nk = 0ull;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) nk = s_next[w] > nk ? s_next[w] : nk;
+      const double a = __longlong_as_double(tk), c = __longlong_as_double(nk);
       const double gap = a > 0.0 ? (a - c) / a : 0.0;
       min_gap = fmin(min_gap, gap);
     }
+    have = f;
     __syncthreads();
   }
   __syncthreads();
