@@ -308,36 +308,20 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
     if k1_events is not None:
         k1_events[1].record()
 
-    # ragged arena plan (device prefix sum); the single device->host read of
-    # the session sizes the arena and brings the profile summary along
+    # Everything the compaction needs except the arena is prepared before the
+    # session's single device->host read (the packed summary, which also
+    # carries the arena size); after it only the arena allocation stands
+    # between the read and the next launches, so the GPU idles briefly.
     seg_cap = torch.empty(G, dtype=i32, device=dev)
     seg_off = torch.empty(G, dtype=torch.int64, device=dev)
     check(lib.akv_plan_segments(G, _ptr(out["kept_count"]), int(max_new_tokens), _ptr(seg_cap),
                                 _ptr(seg_off), _ptr(out["total"]), stream))
-    hsum = summary.cpu()
-    host = {name: view(hsum, name).numpy() for name, _, _ in sections}
-    total_slots = int(host["total"][0])
-    choice = host["choice"].reshape(G, nT).astype(np.int64)
-    if (choice < 0).any():
-        raise ProfilerError("no feasible policy met the threshold")
-    res = ProfileResult(
-        family=family, thresholds=thresholds, recovery=host["recovery"].reshape(G, F),
-        cost=host["cost"].reshape(G, F).astype(np.int64), cosine=host["cosine"].reshape(G, F),
-        choice=choice, kept_count=host["kept_count"].astype(np.int64),
-        last_row_recovery=host["lrr"], topk_gap=host["gap"])
-
     cache = CompressedCache(B, H, d, q.dtype, N, int(max_new_tokens), dev)
-    cache.profile_result = res
     cache.head_atoms = torch.empty(G, dtype=torch.uint8, device=dev)
     cache.head_r_l = torch.empty(G, dtype=f64, device=dev)
     cache.head_r_f = torch.empty(G, dtype=f64, device=dev)
     cache.seg_cap, cache.seg_off = seg_cap, seg_off
     cache.max_cap = int(max(1, ((N + max_new_tokens + 7) // 8) * 8))
-    cache.total_slots = max(total_slots, 1)
-    cache.kc = torch.empty(cache.total_slots, d, dtype=q.dtype, device=dev)
-    cache.vc = torch.empty(cache.total_slots, d, dtype=q.dtype, device=dev)
-    cache.meta = torch.empty(cache.total_slots, dtype=i32, device=dev)
-    cache.score = torch.empty(cache.total_slots, dtype=f64, device=dev)
     cache.live_buf = [torch.empty(G, dtype=i32, device=dev), torch.empty(G, dtype=i32, device=dev)]
     cache.base_live = torch.empty(G, dtype=i32, device=dev)
     cache.out = out["out_last"]
@@ -347,7 +331,6 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
     cache.slopes, cache.sinks = slopes, sinks
     cache.colsum = out["colsum"]
     cache.lastp = out["lastp"]
-
     c = CompactArgs()
     c.B, c.H, c.N, c.d, c.dtype = B, H, N, d, dt
     c.k_dev, c.v_dev, c.ld = _ptr(k), _ptr(v), ld
@@ -362,16 +345,34 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
     c.head_atoms_dev, c.head_r_l_dev, c.head_r_f_dev = (_ptr(cache.head_atoms),
                                                         _ptr(cache.head_r_l), _ptr(cache.head_r_f))
     c.seg_off_dev, c.seg_cap_dev = _ptr(seg_off), _ptr(seg_cap)
+    c.live_dev = _ptr(cache.live_buf[0])
+
+    hsum = summary.cpu()
+    total_slots = int(view(hsum, "total")[0])
+    cache.total_slots = max(total_slots, 1)
+    cache.kc = torch.empty(cache.total_slots, d, dtype=q.dtype, device=dev)
+    cache.vc = torch.empty(cache.total_slots, d, dtype=q.dtype, device=dev)
+    cache.meta = torch.empty(cache.total_slots, dtype=i32, device=dev)
+    cache.score = torch.empty(cache.total_slots, dtype=f64, device=dev)
     c.kc_dev, c.vc_dev, c.meta_dev, c.score_dev = (_ptr(cache.kc), _ptr(cache.vc),
                                                    _ptr(cache.meta), _ptr(cache.score))
-    c.live_dev = _ptr(cache.live_buf[0])
     check(lib.akv_compact(C.byref(c), stream), EngineError)
     cache.base_live.copy_(cache.live_buf[0])  # the decode's live-count bound anchor
-
     ws_bytes = lib.akv_decode_workspace_size(B, H, d, cache.max_cap, cache.total_slots)
     cache.workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     check(lib.akv_decode_workspace_init(_ptr(cache.workspace), ws_bytes, B, H, d, cache.max_cap,
                                         cache.total_slots, stream))
+
+    host = {name: view(hsum, name).numpy() for name, _, _ in sections}
+    choice = host["choice"].reshape(G, nT).astype(np.int64)
+    if (choice < 0).any():
+        raise ProfilerError("no feasible policy met the threshold")
+    res = ProfileResult(
+        family=family, thresholds=thresholds, recovery=host["recovery"].reshape(G, F),
+        cost=host["cost"].reshape(G, F).astype(np.int64), cosine=host["cosine"].reshape(G, F),
+        choice=choice, kept_count=host["kept_count"].astype(np.int64),
+        last_row_recovery=host["lrr"], topk_gap=host["gap"])
+    cache.profile_result = res
     cache._dargs = _decode_args(cache, dt)
     cache.track_recovery = bool(diagnostics)
     # per-head recovery of the latest step; before any decode step it is the
