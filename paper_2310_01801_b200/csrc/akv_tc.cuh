@@ -104,6 +104,36 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2: two lanes of work per issued
+// instruction) for the softmax epilogues.
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// exp2 of both lanes (MUFU)
+__device__ __forceinline__ uint64_t f2_exp2(uint64_t x) {
+  float a, b;
+  f2_unpack(x, a, b);
+  float ya, yb;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ya) : "f"(a));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(yb) : "f"(b));
+  return f2_pack(ya, yb);
+}
+
 // 2^x for x <= 0 on the FMA pipe (MUFU stays free for the other lanes of the
 // work): x = j + f with j = round(x) taken from the mantissa of x + 1.5*2^23,
 // 2^f on [-0.5, 0.5] by a degree-5 minimax polynomial (max relative error
@@ -123,11 +153,40 @@ __device__ __forceinline__ float exp2_fma(float x) {
   return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
 }
 
-// share of the exponentials of the unmasked K1 tiles evaluated on the FMA
-// pipe: every kPolyEvery-th, 0 = none.  Measured on B200 at config 4: a
-// quarter on the FMA pipe left both passes unchanged (5.71 -> 5.73 ms and
-// 6.53 -> 6.83 ms): the epilogue is issue-bound, not MUFU-bound, so it is off.
-constexpr int kPolyEvery = 0;
+// exp2_fma on both lanes of a packed pair: FADD2 / FFMA2 for the rounding
+// split and the polynomial, scalar clamp and exponent insertion
+__device__ __forceinline__ uint64_t f2_exp2_fma(uint64_t x2) {
+  float a, b;
+  f2_unpack(x2, a, b);
+  x2 = f2_pack(fmaxf(a, -125.f), fmaxf(b, -125.f));
+  const uint64_t M = f2_pack(12582912.f, 12582912.f), nM = f2_pack(-12582912.f, -12582912.f);
+  const uint64_t t = f2_add(x2, M);
+  uint64_t f;
+  {
+    float r0, r1, x0, x1;
+    f2_unpack(f2_add(t, nM), r0, r1);
+    f2_unpack(x2, x0, x1);
+    f = f2_add(x2, f2_pack(-r0, -r1));
+  }
+  uint64_t p = f2_pack(1.3264727e-3f, 1.3264727e-3f);
+  p = f2_fma(p, f, f2_pack(9.6715129e-3f, 9.6715129e-3f));
+  p = f2_fma(p, f, f2_pack(5.5507337e-2f, 5.5507337e-2f));
+  p = f2_fma(p, f, f2_pack(2.4022242e-1f, 2.4022242e-1f));
+  p = f2_fma(p, f, f2_pack(6.9314698e-1f, 6.9314698e-1f));
+  p = f2_fma(p, f, f2_pack(1.0f, 1.0f));
+  float p0, p1, t0, t1;
+  f2_unpack(p, p0, p1);
+  f2_unpack(t, t0, t1);
+  return f2_pack(__int_as_float(__float_as_int(p0) + ((__float_as_int(t0) - 0x4B400000) << 23)),
+                 __int_as_float(__float_as_int(p1) + ((__float_as_int(t1) - 0x4B400000) << 23)));
+}
+
+// share of the exponentials of the unmasked row-pass tiles evaluated on the
+// FMA pipe: every kPolyEvery-th pair, 0 = none.  Measured at config 4 (B200):
+// row pass 5.67 -> 5.40 ms with a quarter on the FMA pipe; neither the MUFU
+// (XU ~60 %) nor the issue slots (~64 %) saturate - the epilogue is latency
+// bound at 16 epilogue warps per SM.
+constexpr int kPolyEvery = 4;
 
 __device__ __forceinline__ float exp2_mixed(float x, int c) {
   return (kPolyEvery > 0 && c % (kPolyEvery > 0 ? kPolyEvery : 1) == kPolyEvery - 1)
