@@ -14,9 +14,11 @@
 //   (profiler.py:148-161 cosine), the prompt's last row A[N-1, :] and the
 //   last-row output partial A[N-1, tile] @ V[tile] (engine.py:248,255).
 // Warp roles per CTA (320 threads): warp 0 TMA producer, warp 1 TMEM owner
-// and single-thread MMA issuer, warps 2-9 epilogue in two column halves
-// (warps 2-5 take accumulator columns 0-63, warps 6-9 columns 64-127; the
-// halves merge their per-row / per-key results at the end).  The fixed operand (Q
+// and single-thread MMA issuer, warps 2-9 epilogue in kGroups = 2 column
+// groups of 64 accumulator columns (a group's 4 warps cover the 128 TMEM
+// lanes; the groups merge their per-row / per-key results at the end).
+// Measured at config 4: 4 groups (16 epilogue warps per CTA, 56 registers)
+// is slower (column pass 6.3 -> 7.8 ms).  The fixed operand (Q
 // tile in pass 1, K tile in pass 2) is loaded once; the streamed operand
 // goes through a 2-stage ring.  Grid blocks are ordered heaviest first.
 
@@ -32,8 +34,10 @@ constexpr int kTT = 128;                   // tile edge (queries / keys)
 constexpr int kBoxB = 128 * 128;           // one 128-row x 64-col bf16 box (16 KB)
 constexpr int kTileB = 2 * kBoxB;          // 128 x 128 bf16 tile (32 KB)
 constexpr int kRing = 2;                   // streamed-operand stages
-constexpr int kTcThreads = 320;            // warp0 TMA, warp1 MMA/TMEM, warps 2-9 epilogue
-constexpr int kEpiWarps = 8;
+constexpr int kGroups = 2;                 // epilogue column groups (4 warps = 128 TMEM lanes each)
+constexpr int kCols = 128 / kGroups;       // accumulator columns per epilogue thread and tile
+constexpr int kEpiWarps = 4 * kGroups;
+constexpr int kTcThreads = 64 + 32 * kEpiWarps;  // warp0 TMA, warp1 MMA/TMEM, then the epilogue
 constexpr uint32_t kTmemCols = 256;        // two 128-column fp32 accumulators
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
@@ -55,7 +59,13 @@ struct TcParams {
   float scale;
 };
 
-using EpiSync = NamedSync<256, 1, 64>;
+using EpiSync = NamedSync<32 * kEpiWarps, 1, 64>;
+
+// kCols consecutive fp32 accumulator columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float* v) {
+  if constexpr (kCols == 64) tmem_ld64(taddr, v);
+  else tmem_ld32(taddr, v);
+}
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
@@ -73,17 +83,17 @@ __device__ __forceinline__ void mma_tile(uint32_t tmem_d, const uint8_t* a_tile,
   }
 }
 
-// online (max, sum) update of a row with 64 logits already in the log2
+// online (max, sum) update of a row with kCols logits already in the log2
 // domain (masked entries -inf)
 __device__ __forceinline__ void row_update_scaled(const float* v, float& m, float& l) {
   float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-  for (int c = 0; c < 64; ++c) mx[c & 3] = fmaxf(mx[c & 3], v[c]);
+  for (int c = 0; c < kCols; ++c) mx[c & 3] = fmaxf(mx[c & 3], v[c]);
   const float mn = fmaxf(fmaxf(m, fmaxf(mx[0], mx[1])), fmaxf(mx[2], mx[3]));
   if (mn == -INFINITY) return;
   float sm[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-  for (int c = 0; c < 64; ++c) {
+  for (int c = 0; c < kCols; ++c) {
     const float x = v[c] - mn;
     sm[c & 3] += exp2_mixed(x, c);
   }
@@ -96,13 +106,13 @@ __device__ __forceinline__ void row_update_scaled(const float* v, float& m, floa
 __device__ __forceinline__ void row_update_raw(const float* v, float sl2, float& m, float& l) {
   float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-  for (int c = 0; c < 64; ++c) mx[c & 3] = fmaxf(mx[c & 3], v[c]);
+  for (int c = 0; c < kCols; ++c) mx[c & 3] = fmaxf(mx[c & 3], v[c]);
   const float mn = fmaxf(m, fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * sl2);
   // packed pairs: one FFMA2 and one FADD2 per two exponentials
   const uint64_t s2 = f2_pack(sl2, sl2), nb2 = f2_pack(-mn, -mn);
   uint64_t acc[2] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
 #pragma unroll
-  for (int c = 0; c < 64; c += 2) {
+  for (int c = 0; c < kCols; c += 2) {
     const uint64_t x = f2_fma(f2_pack(v[c], v[c + 1]), s2, nb2);
     const bool poly = kPolyEvery > 0 && (c >> 1) % (kPolyEvery > 0 ? kPolyEvery : 1) == kPolyEvery - 1;
     acc[(c >> 1) & 1] = f2_add(acc[(c >> 1) & 1], poly ? f2_exp2_fma(x) : f2_exp2(x));
@@ -174,10 +184,10 @@ __global__ void __launch_bounds__(kTcThreads, 2)
       }
     }
   } else {  // ---------------- epilogue (warps 2-9) ----------------
-    __shared__ float s_ml[kTT][2];
+    __shared__ float s_ml[kGroups][kTT][2];
     const int quarter = warp & 3;
     const int et = threadIdx.x - 64;
-    const int half = et >> 7;  // accumulator columns [64*half, 64*half + 64)
+    const int half = et >> 7;  // column group: accumulator columns [kCols*half, kCols*(half+1))
     const int rl = quarter * 32 + lane;
     const int row = qt * kTT + rl;
     const float sl2 = p.scale * kLog2e;
@@ -203,18 +213,18 @@ __global__ void __launch_bounds__(kTcThreads, 2)
       }
       mbar_wait(&acc_full[a], (kt >> 1) & 1);
       tc_fence_after();
-      float v[64];
-      tmem_ld64(tmem + ((uint32_t)(quarter * 32) << 16) + a * kTT + half * 64, v);
+      float v[kCols];
+      tmem_ld_cols(tmem + ((uint32_t)(quarter * 32) << 16) + a * kTT + half * kCols, v);
       // the values are in registers: hand the accumulator back to the MMA warp
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[a]);
       const bool masked = (kt == qt) || ((kt + 1) * kTT > p.N);
-      const float* ct = &s_col[a][half * 64];
+      const float* ct = &s_col[a][half * kCols];
       if (masked) {  // diagonal / ragged tile: causal and length masks
-        const int c0 = kt * kTT + half * 64;
+        const int c0 = kt * kTT + half * kCols;
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
+        for (int c = 0; c < kCols; ++c) {
           float y = bias ? fmaf(v[c], sl2, ct[c]) : v[c] * sl2;
           if (c0 + c > row || c0 + c >= p.N) y = -INFINITY;
           v[c] = y;
@@ -222,7 +232,7 @@ __global__ void __launch_bounds__(kTcThreads, 2)
         row_update_scaled(v, m, l);
       } else if (bias) {
 #pragma unroll
-        for (int c = 0; c < 64; c += 4) {
+        for (int c = 0; c < kCols; c += 4) {
           const float4 t = *reinterpret_cast<const float4*>(ct + c);
           v[c] = fmaf(v[c], sl2, t.x);
           v[c + 1] = fmaf(v[c + 1], sl2, t.y);
@@ -234,14 +244,20 @@ __global__ void __launch_bounds__(kTcThreads, 2)
         row_update_raw(v, sl2, m, l);
       }
     }
-    // merge the two column halves of every row
-    if (half == 1) { s_ml[rl][0] = m; s_ml[rl][1] = l; }
+    // merge the column groups of every row
+    s_ml[half][rl][0] = m;
+    s_ml[half][rl][1] = l;
     EpiSync::sync();
     if (half == 0) {
-      const float m2 = s_ml[rl][0], l2 = s_ml[rl][1];
-      const float mm = fmaxf(m, m2);
-      const float ll = (m == -INFINITY ? 0.f : l * fast_exp2(m - mm)) +
-                       (m2 == -INFINITY ? 0.f : l2 * fast_exp2(m2 - mm));
+      float mm = -INFINITY;
+#pragma unroll
+      for (int gq = 0; gq < kGroups; ++gq) mm = fmaxf(mm, s_ml[gq][rl][0]);
+      float ll = 0.f;
+#pragma unroll
+      for (int gq = 0; gq < kGroups; ++gq) {
+        const float m2 = s_ml[gq][rl][0];
+        if (m2 != -INFINITY) ll += s_ml[gq][rl][1] * fast_exp2(m2 - mm);
+      }
       const float rowterm = -slope_l2 * (float)row;
       if (row < p.N) p.lse[(size_t)g * p.N + row] = (mm + rowterm + __log2f(ll)) * kLn2;
     }
@@ -315,11 +331,11 @@ __global__ void __launch_bounds__(kTcThreads, 2)
       }
     }
   } else {  // ---------------- epilogue (warps 2-9) ----------------
-    __shared__ double s_part[2][kTT];
-    __shared__ float s_plast[kTT];
+    __shared__ double s_part[2][kGroups][kTT];
+    __shared__ float s_plast[kGroups][kTT];
     const int quarter = warp & 3;
     const int et = threadIdx.x - 64;
-    const int half = et >> 7;  // query columns [64*half, 64*half + 64) of every tile
+    const int half = et >> 7;  // column group: query columns [kCols*half, kCols*(half+1)) of a tile
     const int kl = quarter * 32 + lane;
     const int key = kt * kTT + kl;
     const float sl2 = p.scale * kLog2e;
@@ -351,19 +367,19 @@ __global__ void __launch_bounds__(kTcThreads, 2)
       EpiSync::sync();
       mbar_wait(&acc_full[a], (i >> 1) & 1);
       tc_fence_after();
-      float v[64];
-      tmem_ld64(tmem + ((uint32_t)(quarter * 32) << 16) + a * kTT + half * 64, v);
+      float v[kCols];
+      tmem_ld_cols(tmem + ((uint32_t)(quarter * 32) << 16) + a * kTT + half * kCols, v);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[a]);
       // diagonal tile (causal mask), ragged tail (q >= N) and the tile holding row N-1
       const bool masked = (i == 0) || ((qt + 1) * kTT > p.N) || (qt == qlast / kTT);
-      const float* ct = &s_col[a][half * 64];
+      const float* ct = &s_col[a][half * kCols];
       float ts[4] = {0.f, 0.f, 0.f, 0.f}, tq[4] = {0.f, 0.f, 0.f, 0.f};
       if (masked) {
-        const int q0 = qt * kTT + half * 64;
+        const int q0 = qt * kTT + half * kCols;
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
+        for (int c = 0; c < kCols; ++c) {
           float pr = fast_exp2(fmaf(v[c], sl2, kterm + ct[c]));
           const int q = q0 + c;
           if (q < key || q >= p.N) pr = 0.f;
@@ -375,7 +391,7 @@ __global__ void __launch_bounds__(kTcThreads, 2)
         dsq += (double)((tq[0] + tq[1]) + (tq[2] + tq[3]));
       } else if (slope_on) {
 #pragma unroll
-        for (int c = 0; c < 64; c += 4) {
+        for (int c = 0; c < kCols; c += 4) {
           const float4 t = *reinterpret_cast<const float4*>(ct + c);
           const float tt[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
@@ -394,7 +410,7 @@ __global__ void __launch_bounds__(kTcThreads, 2)
         uint64_t as = f2_pack(0.f, 0.f), aq = f2_pack(0.f, 0.f);
         uint64_t bs = f2_pack(0.f, 0.f), bq = f2_pack(0.f, 0.f);
 #pragma unroll
-        for (int c = 0; c < 64; c += 4) {
+        for (int c = 0; c < kCols; c += 4) {
           const float4 t = *reinterpret_cast<const float4*>(ct + c);
           const uint64_t p0 = f2_exp2(f2_fma(f2_pack(v[c], v[c + 1]), s2x, f2_pack(t.x, t.y)));
           const uint64_t x1 = f2_fma(f2_pack(v[c + 2], v[c + 3]), s2x, f2_pack(t.z, t.w));
@@ -417,13 +433,16 @@ __global__ void __launch_bounds__(kTcThreads, 2)
         dsq += (double)(s2 * (kfac * kfac));
       }
     }
-    // the last query row lies in the last (masked) tile; merge the halves
-    if (half == 1) { s_part[0][kl] = dsum; s_part[1][kl] = dsq; s_plast[kl] = lastp; }
+    // the last query row lies in the last (masked) tile; merge the groups
+    if (half > 0) { s_part[0][half][kl] = dsum; s_part[1][half][kl] = dsq; s_plast[half][kl] = lastp; }
     EpiSync::sync();
     if (half == 0) {
-      dsum += s_part[0][kl];
-      dsq += s_part[1][kl];
-      lastp += s_plast[kl];
+#pragma unroll
+      for (int gq = 1; gq < kGroups; ++gq) {
+        dsum += s_part[0][gq][kl];
+        dsq += s_part[1][gq][kl];
+        lastp += s_plast[gq][kl];
+      }
       if (key >= p.N) lastp = 0.f;
       if (key < p.N) {
         p.colsum[(size_t)g * p.N + key] = dsum;
