@@ -21,7 +21,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 from paper_2310_01801_b200.workloads import (  # noqa: E402
-    LOCAL_SLOPE, SINK_LOGIT, Workload, config0, config1,
+    LOCAL_SLOPE, SINK_LOGIT, Workload, config0, config1, config4,
 )
 
 ORDER_DEFAULT = ("special", "punct", "frequent", "local")
@@ -54,6 +54,15 @@ def _c1_heads(seed=1) -> Workload:
     return w
 
 
+def _c4_heads(seed=4) -> Workload:
+    """Config-4 shapes (N=16384, d=128, bf16, 256 decode steps) on three
+    heads of batch row 1: two sink heads that compress (special+punct+
+    frequent at T=0.95, evicting at every step) and a local+sink head."""
+    w = config4(seed, B=1)
+    w.name = "c4_heads"
+    return w
+
+
 def c1_heads_subset(w: Workload) -> list:
     planted = [h for h in range(w.H) if w.slopes[h] != 0 or w.sinks[h] != 0]
     plain = [h for h in range(w.H) if h not in planted][:2]
@@ -75,7 +84,12 @@ CASES = {
     "c0_fixed_freq": (_c0_sink, dict(fixed="frequent(r_f=0.25)")),
     "c1_small": (_c1_small, dict(decode_T=0.98)),
     "c1_heads": (_c1_heads, dict(decode_T=0.98, heads="planted+2")),
+    "c4_heads": (_c4_heads, dict(decode_T=0.95, heads=[(1, 0), (1, 3), (1, 18)])),
 }
+
+# cases whose oracle run is too slow for the CPU suite (checked on the GPU
+# against the reference's goldens directly)
+LONG_CASES = ("c4_heads",)
 
 MIXED = dict(name="mixed4x4", prompt_len=64, steps=24, T=0.95, seed=101, dominance=0.97)
 
@@ -93,6 +107,8 @@ def case_heads(w: Workload, opts: dict) -> list:
     """(b, h) pairs of the case, in the reference's sorted grid order."""
     if opts.get("heads") == "planted+2":
         return [(0, h) for h in c1_heads_subset(w)]
+    if isinstance(opts.get("heads"), list):
+        return [tuple(x) for x in opts["heads"]]
     return [(b, h) for b in range(w.B) for h in range(w.H)]
 
 

@@ -7,10 +7,10 @@ import pytest
 import cases as C
 from helpers import load_golden, oracle_case
 
-CPU_CASES = [n for n in C.CASES if n != "c1_heads"]
+CPU_CASES = [n for n in C.CASES if n not in C.LONG_CASES]
 
 
-@pytest.mark.parametrize("name", CPU_CASES + ["c1_heads"])
+@pytest.mark.parametrize("name", CPU_CASES)
 def test_oracle_matches_reference_golden(name):
     g = load_golden(name)
     o = oracle_case(name)
