@@ -185,10 +185,70 @@ class CompressedCache:
         """Latest attention output per head, fp32 [B, H, d]."""
         return self.out
 
+    @property
+    def heads(self) -> dict:
+        """Host snapshot of every head's state in the reference's layout
+        (engine.py:100-117 HeadCacheState), keyed by the model grid's
+        (layer, head) keys (or (b, h) for tensor-level caches): live
+        positions ascending (the reference keeps attended order, which is
+        ascending), their K/V rows, the score sidecar, the pending output and
+        the latest recovery.  ``scores`` is full length with NaN at evicted
+        positions (the reference keeps their frozen values; only live slots
+        take part in later decisions).  One device->host copy per call."""
+        keys = self.keys or [(b, h) for b in range(self.B) for h in range(self.H)]
+        live = self.live.cpu().numpy()
+        off = self.seg_off.cpu().numpy()
+        meta = self.meta.cpu().numpy()
+        kc = self.kc.float().cpu().numpy()
+        vc = self.vc.float().cpu().numpy()
+        score = self.score.cpu().numpy()
+        out = self.out.reshape(self.G, -1).double().cpu().numpy()
+        rec = self.step_recovery.cpu().numpy()
+        atoms = self.head_atoms.cpu().numpy()
+        fam = self.profile_result.family if self.profile_result is not None else ()
+        by_bits = {pol.bits: pol for pol in fam}
+        states = {}
+        for g, key in enumerate(keys):
+            sl = slice(int(off[g]), int(off[g]) + int(live[g]))
+            pos = meta[sl] & ((1 << 24) - 1)
+            order = np.argsort(pos, kind="stable")
+            freq = bool(atoms[g] & 4) and not bool(atoms[g] & 16)
+            scores = None
+            if freq:
+                scores = np.full(self.seq_len, np.nan)
+                scores[pos] = score[sl]
+            states[key] = HeadCacheState(
+                policy=self.profile.decisions[key].policy if (self.profile is not None and
+                                                              key in self.profile.decisions)
+                else by_bits.get(int(atoms[g])),
+                positions=[int(p) for p in pos[order]], K=kc[sl][order], V=vc[sl][order],
+                scores=scores, pending_output=out[g], last_row_recovery=float(rec[g]))
+        return states
+
     def check(self):
         st = int(self.status.item())
         if st != 0:
             raise _lib.AkvError(st, "decode overflowed a cache segment (capacity exceeded)")
+
+
+@dataclass
+class HeadCacheState:
+    """One head's compressed state (engine.py:100-117), as a host snapshot."""
+
+    policy: CompressionPolicy | None
+    positions: list
+    K: np.ndarray
+    V: np.ndarray
+    scores: np.ndarray | None
+    pending_output: np.ndarray
+    last_row_recovery: float
+
+    @property
+    def sidecar(self):
+        """Cumulative scores of the retained positions (engine.py:112-117)."""
+        if self.scores is None:
+            return None
+        return self.scores[np.asarray(self.positions, dtype=np.intp)]
 
 
 def _family_arrays(family, args):
