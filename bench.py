@@ -327,9 +327,100 @@ def bench_ours(args):
         "wall_s": t_wall,
         "e2e": e2e,
     }
+    if world == 1 and not args.no_extras:
+        del qd, kd, vd, cd, dec
+        torch.cuda.empty_cache()
+        line["other_configs"] = bench_extras(T, dev, peaks)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_port(w, T)
     print(json.dumps(line), flush=True)
+
+
+def bench_extras(T, dev, peaks):
+    """Supplementary single-GPU measurements of BASELINE configs 4 and 2 (not
+    the headline): one timed c4 session (long context, N=16384) and a c2
+    decode (32-layer Llama-7B shape through the multi-layer caller)."""
+    import torch
+
+    from paper_2310_01801_b200 import ProfilerConfig
+    from paper_2310_01801_b200.workloads import config4
+
+    out = {}
+    w = config4()
+    qd, kd, vd, cd, *_ = make_inputs(w, dev)
+    slopes = torch.tensor(w.slopes, dtype=torch.float32, device=dev)
+    sinks = torch.tensor(w.sinks, dtype=torch.float32, device=dev)
+    N, D = w.N, w.D
+    dec = ([qd[:, :, N + t] for t in range(D)], [kd[:, :, N + t] for t in range(D)],
+           [vd[:, :, N + t] for t in range(D)], [cd[:, N + t].contiguous() for t in range(D)])
+    res, cache, lives = run_session(w, T, qd, kd, vd, cd, slopes, sinks, dec, record=True)
+    cache.check()
+    nbytes = decode_bytes(w, res, lives)
+    del cache
+    run_session(w, T, qd, kd, vd, cd, slopes, sinks, dec)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    res, cache, _ = run_session(w, T, qd, kd, vd, cd, slopes, sinks, dec, ev=ev)
+    torch.cuda.synchronize()
+    enc, decm = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
+    fam = res.family
+    pol = np.bincount(res.choice[:, 0], minlength=len(fam))
+    gbs = statistics.mean(nbytes) / (decm * 1e-3 / D) / 1e9
+    out["c4"] = {
+        "workload": f"long context: B={w.B} H={w.H} d={w.d} N={N} D={D} bf16, T={T:g}",
+        "session_tok_s": w.B * D / ((enc + decm) * 1e-3), "profiling_ms": enc,
+        "k1_tflops_incl_policy_and_compaction": 2.0 * w.B * w.H * w.d * N * (N + 1) / (enc * 1e-3) / 1e12,
+        "decode_us_per_step": decm * 1e3 / D, "decode_achieved_gbs": gbs,
+        "decode_frac_of_hbm_peak": gbs / peaks.get("hbm_gbs"),
+        "pruned_ratio_end": 1.0 - cache.total_retained() / float(w.B * w.H * (N + D)),
+        "policies": {str(fam[i]): int(pol[i]) for i in range(len(fam)) if pol[i]},
+    }
+    del qd, kd, vd, cd, dec, cache
+    torch.cuda.empty_cache()
+
+    from paper_2310_01801_b200.llama import LLAMA_7B, FastGenLlama
+
+    B, N, D = 16, 2048, 512
+    model = FastGenLlama(LLAMA_7B, seed=0, max_positions=N + D + 8)
+    rng = np.random.default_rng([0, 2])
+    from paper_2310_01801_b200.workloads import PUNCT_IDS, PUNCT_PROB, SPECIAL_IDS
+
+    ids = rng.integers(0, LLAMA_7B.vocab, size=(B, N))
+    punct = rng.random((B, N)) < PUNCT_PROB
+    ids = np.where(punct, np.asarray(PUNCT_IDS)[rng.integers(0, len(PUNCT_IDS), (B, N))], ids)
+    ids[:, 0] = SPECIAL_IDS[0]
+    tokens = torch.from_numpy(ids).to(dev)
+    pc = ProfilerConfig(recovery_threshold=T)
+    model.prefill(tokens, pc, max_new_tokens=D)          # warm-up (allocator, cuBLAS, graphs)
+    for _ in range(8):
+        model.decode_step()
+    model.caches = []
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    e[0].record()
+    pre = model.prefill(tokens, pc, max_new_tokens=D)
+    e[1].record()
+    for _ in range(D):
+        model.decode_step()
+    e[2].record()
+    torch.cuda.synchronize()
+    model.check()
+    pre_ms, dec_ms = e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2])
+    cfg = LLAMA_7B
+    wbytes = 2 * (cfg.n_layers * (4 * cfg.d_model * cfg.d_model + 3 * cfg.d_model * cfg.ffn)
+                  + cfg.vocab * cfg.d_model)
+    kv = 2 * cfg.n_layers * B * cfg.n_heads * cfg.head_dim * 2 * (N + D / 2)  # mean live rows
+    step_s = dec_ms * 1e-3 / D
+    out["c2"] = {
+        "workload": f"Llama-7B shape, 32 layers, random bf16 weights, B={B} prompt {N} greedy "
+                    f"decode {D}, T={T:g}",
+        "decode_tok_s": B * D / (dec_ms * 1e-3), "decode_ms_per_step": dec_ms / D,
+        "prefill_ms": pre_ms, "profiling_ms_per_layer": float(np.mean(pre.profiling_ms())),
+        "step_hbm_bytes": wbytes + kv, "step_achieved_gbs": (wbytes + kv) / step_s / 1e9,
+        "step_frac_of_hbm_peak": (wbytes + kv) / step_s / 1e9 / peaks.get("hbm_gbs"),
+        "cache_tokens_end": model.cache_tokens(),
+    }
+    del model
+    torch.cuda.empty_cache()
+    return out
 
 
 def bench_e2e(w, T, args, qh, kh, vh, clsh, slopes, sinks, dev, dist):
@@ -543,6 +634,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--T", type=float, default=0.95)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the supplementary config-4 / config-2 measurements")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
