@@ -198,6 +198,15 @@ typedef struct akv_decode_args {
   int32_t flags;                 /* AKV_DECODE_* */
   float* lse_out_dev;            /* optional [B*H] natural-log log-sum-exp of each head's attended
                                     logits (live slots + the new token), for diagnostics */
+  void* const* peer_out_dev;     /* optional device array of n_peers pointers, each to a
+                                    [B, peer_ld] buffer (cache dtype) that receives this call's
+                                    head outputs at columns peer_col0 + h*d: the cross-shard
+                                    gather of a head-sharded layer fused into the combine
+                                    (peer pointers from CUDA IPC / symmetric memory; the caller
+                                    barriers before reading) */
+  int32_t n_peers;
+  int64_t peer_ld;
+  int64_t peer_col0;
 } akv_decode_args;
 
 /* akv_decode_args.flags: the previous kernel on the stream is this cache's

@@ -66,7 +66,8 @@ class DecodeArgs(C.Structure):
         ("vc_dev", P), ("meta_dev", P), ("score_dev", P), ("base_live_dev", P), ("live_in_dev", P),
         ("live_out_dev", P), ("out_dev", P), ("evicted_dev", P), ("status_dev", P),
         ("max_cap", i32), ("total_slots", i64), ("workspace_dev", P), ("workspace_bytes", sz),
-        ("pos_dev", P), ("flags", i32), ("lse_out_dev", P),
+        ("pos_dev", P), ("flags", i32), ("lse_out_dev", P), ("peer_out_dev", P),
+        ("n_peers", i32), ("peer_ld", i64), ("peer_col0", i64),
     ]
 
 

@@ -91,6 +91,10 @@ struct DecParams {
   const int32_t* pos_dev;     // device position (CUDA-graph replays), overrides pos
   int flags;                  // AKV_DECODE_* flags
   float* lse_out;             // [G] log-sum-exp of each head's attended logits, or NULL
+  void* const* peer_out;      // [n_peers] buffers [B, peer_ld] receiving o (cache dtype)
+  int n_peers;
+  int64_t peer_ld, peer_col0;
+  int peer_bf16;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -603,6 +607,25 @@ __device__ void head_epilogue(const DecParams& p, const HeadCtx& hc, int nparts,
       if (t < D) p.out[(size_t)g * D + t] = acc[u] * inv;
     }
     if (p.lse_out && tid == 0) p.lse_out[g] = gM + logf(gl);
+    // the head's output row also goes straight into every peer's gathered
+    // [B, H_total*d] buffer (the cross-shard gather of a head-sharded model
+    // layer, fused into the combine: no separate collective, no cast)
+    if (p.n_peers > 0) {
+      const int b = g / p.H, h = g % p.H;
+      const int64_t off = (int64_t)b * p.peer_ld + p.peer_col0 + (int64_t)h * D;
+      for (int r = 0; r < p.n_peers; ++r) {
+        void* base = p.peer_out[r];
+#pragma unroll
+        for (int u = 0; u < DPT; ++u) {
+          const int t = tid + u * NC;
+          if (t >= D) continue;
+          if (p.peer_bf16)
+            static_cast<__nv_bfloat16*>(base)[off + t] = __float2bfloat16_rn(acc[u] * inv);
+          else
+            static_cast<float*>(base)[off + t] = acc[u] * inv;
+        }
+      }
+    }
   }
   if (hc.atoms & AKV_ATOM_FULL) {  // the full cache never evicts
     if (tid == 0) {
@@ -1390,6 +1413,10 @@ extern "C" int akv_decode_step(const akv_decode_args* a, void* stream) {
   if (a->live_in_dev == a->live_out_dev)
     return set_error(AKV_ERR_INVALID, "akv_decode_step: live_in and live_out must be distinct buffers");
   if (a->bh_stride < a->d) return set_error(AKV_ERR_INVALID, "akv_decode_step: bh_stride < d");
+  if (a->n_peers < 0 || (a->n_peers > 0 && (!a->peer_out_dev || a->peer_ld < a->peer_col0 +
+                                                                    (int64_t)a->H * a->d)))
+    return set_error(AKV_ERR_INVALID, "akv_decode_step: bad peer output (n_peers %d, ld %lld)",
+                     a->n_peers, (long long)a->peer_ld);
   DecWs w = carve(a->workspace_dev, a->B, a->H, a->d, a->max_cap, a->total_slots);
   if (a->workspace_bytes < w.bytes) return set_error(AKV_ERR_CAPACITY, "akv_decode_step: workspace too small");
   DecParams p{a->B, a->H, a->B * a->H, a->prompt_len, a->pos, a->q_dev, a->k_dev, a->v_dev,
@@ -1399,7 +1426,8 @@ extern "C" int akv_decode_step(const akv_decode_args* a, void* stream) {
               a->out_dev,
               a->evicted_dev, a->status_dev ? a->status_dev : w.status, w.part, w.logit, w.counter,
               w.max_parts, (float)(1.0 / sqrt((double)a->d)), g_dec_trace, a->pos_dev, a->flags,
-              a->lse_out_dev};
+              a->lse_out_dev, a->peer_out_dev, a->n_peers, a->peer_ld, a->peer_col0,
+              a->dtype == AKV_DTYPE_BF16};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaErrorInvalidValue;
   bool ok = true;

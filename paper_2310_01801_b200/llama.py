@@ -242,6 +242,49 @@ class FastGenLlama:
                                   _stream()), EngineError)
 
     # -- collectives --------------------------------------------------------
+    def _setup_decode_gather(self, B):
+        """Decode-time attention outputs go straight from K3's combine into
+        the O projection's input [B, width] (cache dtype): the local buffer,
+        or - head-sharded over ranks (gather mode) - every rank's
+        symmetric-memory buffer at this rank's column block, followed by a
+        device-side barrier (the cross-shard gather fused into the decode
+        kernel; no NCCL call and no cast on the decode path).  Two buffers
+        alternate between layers so one barrier per layer suffices."""
+        d = self.cfg.head_dim
+        sharded = self.plan.mode == "gather" and self.plan.world > 1
+        width = (self.plan.world * self.Hl * d) if sharded else self.Hl * d
+        col0 = self.plan.rank * self.Hl * d if sharded else 0
+        self._gather_hdl = [None, None]
+        if sharded and self.plan.comm:
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm_mem
+
+            group = self.group if self.group is not None else dist.group.WORLD
+            bufs, ptrs = [], []
+            for i in range(2):
+                t = symm_mem.empty((B, width), dtype=self.dtype, device=self.device)
+                hdl = symm_mem.rendezvous(t, group.group_name)
+                bufs.append(t)
+                ptrs.append(torch.tensor(list(hdl.buffer_ptrs), dtype=torch.int64,
+                                         device=self.device))
+                self._gather_hdl[i] = hdl
+        else:
+            bufs = [torch.zeros(B, width, dtype=self.dtype, device=self.device) for _ in range(2)]
+            ptrs = [torch.tensor([t.data_ptr()], dtype=torch.int64, device=self.device) for t in bufs]
+        self._gather_bufs, self._gather_ptrs = bufs, ptrs
+        for li, c in enumerate(self.caches):
+            a = c._dargs
+            a.peer_out_dev = C.c_void_p(ptrs[li & 1].data_ptr())
+            a.n_peers = ptrs[li & 1].numel()
+            a.peer_ld, a.peer_col0 = width, col0
+
+    def _decode_gathered(self, li):
+        """The O projection's input of layer li after its decode step."""
+        hdl = self._gather_hdl[li & 1]
+        if hdl is not None:
+            hdl.barrier(channel=li & 1)
+        return self._gather_bufs[li & 1]
+
     def _gather_heads(self, o):
         """[rows, Hl*d] local head outputs -> [rows, H*d] (rank-ordered head
         blocks = global head order)."""
@@ -341,6 +384,7 @@ class FastGenLlama:
         self.k1, self.v1 = torch.empty_like(self.q1), torch.empty_like(self.q1)
         self.o_dec = torch.empty(len(self.layers), B, self.Hl, d, dtype=torch.float32,
                                  device=self.device)
+        self._setup_decode_gather(B)
         out = PrefillResult(profiles, self.next_tok)
         out.events = prof_events
         return out
@@ -392,8 +436,7 @@ class FastGenLlama:
                     rec.append((self.q1.clone(), self.k1.clone(), self.v1.clone()))
                 o = decode_step_tensors(self.caches[li], self.q1, self.k1, self.v1, new_cls,
                                         out=self.o_dec[li])
-            o = self._gather_heads(o.view(B, self.Hl * d).to(self.dtype))
-            attn = self._reduce(torch.nn.functional.linear(o, L.wo))
+            attn = self._reduce(torch.nn.functional.linear(self._decode_gathered(li), L.wo))
             delta = self._mlp(L, residual, attn)
         xf = self._rmsnorm(residual, self.final_norm, x=delta)
         logits = torch.nn.functional.linear(xf, self.lm_head)

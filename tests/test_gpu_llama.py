@@ -226,3 +226,35 @@ def test_caller_kernels_vs_torch(dtype):
     assert int(m.next_tok[2]) == 10 and int(m.next_cls[3]) == 2
     assert torch.equal(m.next_cls, m.lut[ref_tok])
     assert torch.equal(m.x_next, m.embed[ref_tok])
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_decode_writes_outputs_to_peer_buffers(dtype):
+    """akv_decode_args.peer_out_dev: the combine writes each head's output row
+    into every listed [B, peer_ld] buffer at columns peer_col0 + h*d (the
+    fused cross-shard gather); here two local buffers stand in for two ranks."""
+    import ctypes as C
+
+    from paper_2310_01801_b200 import ProfilerConfig, decode_step_tensors, encode_prompt_tensors
+
+    g = torch.Generator(device="cuda").manual_seed(3)
+    B, H, N, D, d = 2, 4, 96, 3, 128
+    q, k, v = (torch.randn(B, H, N + D, d, device="cuda", generator=g).to(dtype) for _ in range(3))
+    cls = torch.zeros(B, N + D, dtype=torch.uint8, device="cuda")
+    cls[:, 0] = 1
+    _, cache = encode_prompt_tensors(q, k, v, cls, ProfilerConfig(recovery_threshold=0.9),
+                                     prompt_len=N, max_new_tokens=D)
+    width, col0 = 3 * H * d, H * d          # this "rank" owns the middle block
+    bufs = [torch.full((B, width), -7.0, dtype=dtype, device="cuda") for _ in range(2)]
+    ptrs = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
+    a = cache._dargs
+    a.peer_out_dev, a.n_peers, a.peer_ld, a.peer_col0 = C.c_void_p(ptrs.data_ptr()), 2, width, col0
+    for t in range(D):
+        o = decode_step_tensors(cache, q[:, :, N + t], k[:, :, N + t], v[:, :, N + t],
+                                cls[:, N + t].contiguous())
+        torch.cuda.synchronize()
+        for buf in bufs:
+            got = buf[:, col0:col0 + H * d].float().view(B, H, d)
+            ref = o.to(dtype).float()
+            assert torch.equal(got, ref)
+            assert (buf[:, :col0] == -7).all() and (buf[:, col0 + H * d:] == -7).all()
