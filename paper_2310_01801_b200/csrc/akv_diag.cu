@@ -76,7 +76,7 @@ __device__ __forceinline__ void mass_merge(Mass& s, const Mass& o) {
 }
 
 template <typename T, int D>
-__global__ void __launch_bounds__(kDiagThreads) k_decode_recovery(akv_diag_args a, DiagWs w) {
+__global__ void __launch_bounds__(kDiagThreads, 4) k_decode_recovery(akv_diag_args a, DiagWs w) {
   __shared__ Mass s_red[kDiagThreads / 32];
   __shared__ uint32_t s_bits[kChunk / 32];
   constexpr int PER = Elem<T>::kPerVec;   // elements per 16-byte vector
