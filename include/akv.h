@@ -157,6 +157,18 @@ int akv_plan_segments(int32_t G, const int32_t* kept_count_dev, int32_t extra,
                       int32_t* seg_cap_dev, int64_t* seg_off_dev, int64_t* total_dev,
                       void* stream);
 
+/* The same plan carved from a device-side arena pool (bump allocator over
+ * [0, pool_slots) slots of caller-owned kc/vc/meta/score arrays): this call's
+ * segments start at base = atomicAdd(*pool_used_dev, total), so the
+ * compaction can follow without any host read.  If the pool cannot hold them,
+ * every seg_cap is 0 (compaction and decode skip the heads) and *status_dev =
+ * AKV_ERR_CAPACITY.  Resetting *pool_used_dev (stream-ordered) frees the
+ * pool. */
+int akv_plan_segments_pool(int32_t G, const int32_t* kept_count_dev, int32_t extra,
+                           int32_t* seg_cap_dev, int64_t* seg_off_dev, int64_t* total_dev,
+                           unsigned long long* pool_used_dev, int64_t pool_slots,
+                           int32_t* status_dev, void* stream);
+
 /* ---- K3: one decode step over the compressed cache ------------------- */
 typedef struct akv_decode_args {
   int32_t B, H, d;

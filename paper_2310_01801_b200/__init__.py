@@ -10,7 +10,7 @@ calls fail unless an sm_100 device is present.  There is no CPU fallback.
 from ._lib import AkvError, lib as _lib_handle  # noqa: F401  (loads the .so)
 from .attention import (AttentionError, AttentionMap, causal_attention, softmax_rows,
                         softmax_vector)
-from .engine import (CompressedCache, EngineError, GenerationConfig, GenerationResult,
+from .engine import (ArenaPool, CompressedCache, EngineError, GenerationConfig, GenerationResult,
                      HeadCacheState,
                      GreedyArgmax, Nucleus, ProfileResult, StepRecord, decode_step_tensors,
                      encode_prompt, encode_prompt_tensors, generate, generate_fixed_baseline,

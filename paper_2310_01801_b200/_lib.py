@@ -101,6 +101,7 @@ class DiagArgs(C.Structure):
 # every symbol include/akv.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "akv_profile_workspace_size", "akv_profile", "akv_compact", "akv_plan_segments",
+    "akv_plan_segments_pool",
     "akv_decode_workspace_size", "akv_decode_step", "akv_decode_workspace_init",
     "akv_decode_recovery", "akv_decode_recovery_workspace_size",
     "akv_decode_recovery_workspace_init",
@@ -125,6 +126,8 @@ def _load():
     lib.akv_compact.argtypes = [C.POINTER(CompactArgs), P]
     lib.akv_plan_segments.restype = C.c_int
     lib.akv_plan_segments.argtypes = [i32, P, i32, P, P, P, P]
+    lib.akv_plan_segments_pool.restype = C.c_int
+    lib.akv_plan_segments_pool.argtypes = [i32, P, i32, P, P, P, P, i64, P, P]
     lib.akv_decode_workspace_size.restype = sz
     lib.akv_decode_workspace_size.argtypes = [i32, i32, i32, i32, i64]
     lib.akv_decode_step.restype = C.c_int

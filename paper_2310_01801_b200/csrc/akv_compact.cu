@@ -110,9 +110,61 @@ __global__ void __launch_bounds__(kPlanThreads) k2_plan(int G, const int32_t* ke
   if (threadIdx.x == 0) *total = tot;
 }
 
+// The same plan carved from a device-side arena pool (bump allocator): the
+// segments of this call start at base = atomicAdd(pool_used, total), so no
+// host read is needed before the compaction.  A pool that cannot hold them
+// zeroes every capacity (compaction and decode then skip the heads) and
+// flags AKV_ERR_CAPACITY.
+__global__ void __launch_bounds__(kPlanThreads) k2_plan_pool(int G, const int32_t* kept,
+                                                             int32_t extra, int32_t* cap,
+                                                             int64_t* off, int64_t* total,
+                                                             unsigned long long* pool_used,
+                                                             int64_t pool_slots, int32_t* status) {
+  __shared__ int red[kPlanThreads / 32 + 1];
+  __shared__ long long s_base;
+  const int per = (G + blockDim.x - 1) / blockDim.x;
+  const int lo = min(G, (int)threadIdx.x * per), hi = min(G, lo + per);
+  int mine = 0;
+  for (int g = lo; g < hi; ++g) mine += ((kept[g] + extra + 7) / 8) * 8;
+  int tot;
+  int acc = block_exclusive_scan(mine, red, &tot);
+  if (threadIdx.x == 0) {
+    const unsigned long long b = atomicAdd(pool_used, (unsigned long long)tot);
+    if ((long long)(b + tot) > pool_slots) {
+      atomicExch(status, AKV_ERR_CAPACITY);
+      s_base = -1;
+    } else {
+      s_base = (long long)b;
+    }
+    *total = tot;
+  }
+  __syncthreads();
+  const long long base = s_base;
+  for (int g = lo; g < hi; ++g) {
+    const int c = ((kept[g] + extra + 7) / 8) * 8;
+    cap[g] = base < 0 ? 0 : c;
+    off[g] = base < 0 ? 0 : base + acc;
+    acc += c;
+  }
+}
+
 }  // namespace akv
 
 using namespace akv;
+
+extern "C" int akv_plan_segments_pool(int32_t G, const int32_t* kept_count_dev, int32_t extra,
+                                      int32_t* seg_cap_dev, int64_t* seg_off_dev,
+                                      int64_t* total_dev, unsigned long long* pool_used_dev,
+                                      int64_t pool_slots, int32_t* status_dev, void* stream) {
+  if (G < 1 || extra < 0 || !pool_used_dev || !status_dev || pool_slots < 1)
+    return set_error(AKV_ERR_INVALID, "akv_plan_segments_pool: bad arguments");
+  k2_plan_pool<<<1, kPlanThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      G, kept_count_dev, extra, seg_cap_dev, seg_off_dev, total_dev, pool_used_dev, pool_slots,
+      status_dev);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(AKV_ERR_CUDA, "akv_plan_segments_pool: %s", cudaGetErrorString(e));
+  return AKV_OK;
+}
 
 extern "C" int akv_plan_segments(int32_t G, const int32_t* kept_count_dev, int32_t extra,
                                  int32_t* seg_cap_dev, int64_t* seg_off_dev, int64_t* total_dev,

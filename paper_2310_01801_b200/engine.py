@@ -170,6 +170,7 @@ class CompressedCache:
     def retained_positions(self, g: int | None = None):
         """Sorted live positions of head g (or a list for all heads); one
         device->host copy per call (diagnostics only)."""
+        self.check()
         live = self.live.cpu().numpy()
         off = self.seg_off.cpu().numpy()
         meta = self.meta.cpu().numpy()
@@ -195,6 +196,7 @@ class CompressedCache:
         the latest recovery.  ``scores`` is full length with NaN at evicted
         positions (the reference keeps their frozen values; only live slots
         take part in later decisions).  One device->host copy per call."""
+        self.check()
         keys = self.keys or [(b, h) for b in range(self.B) for h in range(self.H)]
         live = self.live.cpu().numpy()
         off = self.seg_off.cpu().numpy()
@@ -228,7 +230,8 @@ class CompressedCache:
     def check(self):
         st = int(self.status.item())
         if st != 0:
-            raise _lib.AkvError(st, "decode overflowed a cache segment (capacity exceeded)")
+            raise _lib.AkvError(st, "capacity exceeded: a cache segment or the arena pool "
+                                    "cannot hold the retained rows")
 
 
 @dataclass
@@ -251,6 +254,52 @@ class HeadCacheState:
         return self.scores[np.asarray(self.positions, dtype=np.intp)]
 
 
+class ArenaPool:
+    """Device memory for compressed caches with a device-side bump allocator
+    (``akv_plan_segments_pool``): ``encode_prompt_tensors(..., pool=pool)``
+    carves its ragged segments from the pool without the host read that sizes
+    a private arena, so profiling, compaction and decoding are enqueued
+    back to back.  ``reset()`` (stream-ordered) releases every segment carved
+    so far; a session that does not fit flags a capacity error
+    (``CompressedCache.check``)."""
+
+    def __init__(self, slots: int, d: int, dtype=torch.bfloat16, device=None):
+        dev = torch.device("cuda") if device is None else torch.device(device)
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.slots, self.d, self.dtype, self.device = int(slots), int(d), dtype, dev
+        self.kc = torch.empty(self.slots, d, dtype=dtype, device=dev)
+        self.vc = torch.empty(self.slots, d, dtype=dtype, device=dev)
+        self.meta = torch.empty(self.slots, dtype=torch.int32, device=dev)
+        self.score = torch.empty(self.slots, dtype=torch.float64, device=dev)
+        self.used = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def reset(self):
+        self.used.zero_()
+
+    def used_slots(self) -> int:
+        return int(self.used.item())
+
+
+class _PendingProfile:
+    """A ProfileResult whose device->host copy is still in flight (pool
+    sessions): materialised, and any profiling error raised, on first use."""
+
+    def __init__(self, build, event):
+        self._build, self._event, self._res = build, event, None
+
+    def _get(self):
+        if self._res is None:
+            self._event.synchronize()
+            self._res = self._build()
+        return self._res
+
+    def __getattr__(self, name):
+        if name.startswith("_"):
+            raise AttributeError(name)
+        return getattr(self._get(), name)
+
+
 def _family_arrays(family, args):
     if len(family) > _lib.MAX_FAMILY:
         raise ProfilerError(f"feasible family longer than {_lib.MAX_FAMILY} policies")
@@ -265,7 +314,7 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
                           fixed_policy: CompressionPolicy | None = None, *, prompt_len=None,
                           max_new_tokens: int = 0, extra_thresholds=(), slopes=None,
                           sinks=None, diagnostics: bool = False, local_len: int = 0,
-                          k1_events=None):
+                          k1_events=None, pool: ArenaPool | None = None):
     """Profile, select and compact every head of a batch (Alg. 1,
     engine.py:203-272) on the GPU.
 
@@ -280,6 +329,10 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
     shadow keys, engine.py:260-261) so that each decode step reports the
     recovery of its attended set against uncompressed attention
     (``cache.step_recovery``, engine.py:341-349).
+
+    ``pool``: carve the compressed cache from an ArenaPool instead of a
+    private arena sized by a host read; the returned ProfileResult then
+    materialises lazily (its host copy overlaps the compaction and decoding).
     """
     if profiler_cfg is None and fixed_policy is None:
         raise EngineError("need a profiler config or a fixed policy")
@@ -374,9 +427,17 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
     # between the read and the next launches, so the GPU idles briefly.
     seg_cap = torch.empty(G, dtype=i32, device=dev)
     seg_off = torch.empty(G, dtype=torch.int64, device=dev)
-    check(lib.akv_plan_segments(G, _ptr(out["kept_count"]), int(max_new_tokens), _ptr(seg_cap),
-                                _ptr(seg_off), _ptr(out["total"]), stream))
     cache = CompressedCache(B, H, d, q.dtype, N, int(max_new_tokens), dev)
+    cache.status = torch.zeros(1, dtype=i32, device=dev)
+    if pool is None:
+        check(lib.akv_plan_segments(G, _ptr(out["kept_count"]), int(max_new_tokens),
+                                    _ptr(seg_cap), _ptr(seg_off), _ptr(out["total"]), stream))
+    else:
+        if pool.d != d or pool.dtype != q.dtype or pool.device != dev:
+            raise EngineError("arena pool does not match the cache's head dim / dtype / device")
+        check(lib.akv_plan_segments_pool(G, _ptr(out["kept_count"]), int(max_new_tokens),
+                                         _ptr(seg_cap), _ptr(seg_off), _ptr(out["total"]),
+                                         _ptr(pool.used), pool.slots, _ptr(cache.status), stream))
     cache.head_atoms = torch.empty(G, dtype=torch.uint8, device=dev)
     cache.head_r_l = torch.empty(G, dtype=f64, device=dev)
     cache.head_r_f = torch.empty(G, dtype=f64, device=dev)
@@ -386,7 +447,6 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
     cache.base_live = torch.empty(G, dtype=i32, device=dev)
     cache.out = out["out_last"]
     cache.evicted = torch.zeros(G, dtype=i32, device=dev)
-    cache.status = torch.zeros(1, dtype=i32, device=dev)
     cache.classes = classes
     cache.slopes, cache.sinks = slopes, sinks
     cache.colsum = out["colsum"]
@@ -407,13 +467,22 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
     c.seg_off_dev, c.seg_cap_dev = _ptr(seg_off), _ptr(seg_cap)
     c.live_dev = _ptr(cache.live_buf[0])
 
-    hsum = summary.cpu()
-    total_slots = int(view(hsum, "total")[0])
-    cache.total_slots = max(total_slots, 1)
-    cache.kc = torch.empty(cache.total_slots, d, dtype=q.dtype, device=dev)
-    cache.vc = torch.empty(cache.total_slots, d, dtype=q.dtype, device=dev)
-    cache.meta = torch.empty(cache.total_slots, dtype=i32, device=dev)
-    cache.score = torch.empty(cache.total_slots, dtype=f64, device=dev)
+    if pool is None:
+        hsum = summary.cpu()
+        total_slots = int(view(hsum, "total")[0])
+        cache.total_slots = max(total_slots, 1)
+        cache.kc = torch.empty(cache.total_slots, d, dtype=q.dtype, device=dev)
+        cache.vc = torch.empty(cache.total_slots, d, dtype=q.dtype, device=dev)
+        cache.meta = torch.empty(cache.total_slots, dtype=i32, device=dev)
+        cache.score = torch.empty(cache.total_slots, dtype=f64, device=dev)
+    else:
+        hsum = torch.empty(summary.numel(), dtype=torch.uint8, pin_memory=True)
+        hsum.copy_(summary, non_blocking=True)
+        summary_ready = torch.cuda.Event()
+        summary_ready.record()
+        cache.total_slots = pool.slots
+        cache.kc, cache.vc, cache.meta, cache.score = pool.kc, pool.vc, pool.meta, pool.score
+        cache.pool = pool
     c.kc_dev, c.vc_dev, c.meta_dev, c.score_dev = (_ptr(cache.kc), _ptr(cache.vc),
                                                    _ptr(cache.meta), _ptr(cache.score))
     check(lib.akv_compact(C.byref(c), stream), EngineError)
@@ -423,15 +492,18 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
     check(lib.akv_decode_workspace_init(_ptr(cache.workspace), ws_bytes, B, H, d, cache.max_cap,
                                         cache.total_slots, stream))
 
-    host = {name: view(hsum, name).numpy() for name, _, _ in sections}
-    choice = host["choice"].reshape(G, nT).astype(np.int64)
-    if (choice < 0).any():
-        raise ProfilerError("no feasible policy met the threshold")
-    res = ProfileResult(
-        family=family, thresholds=thresholds, recovery=host["recovery"].reshape(G, F),
-        cost=host["cost"].reshape(G, F).astype(np.int64), cosine=host["cosine"].reshape(G, F),
-        choice=choice, kept_count=host["kept_count"].astype(np.int64),
-        last_row_recovery=host["lrr"], topk_gap=host["gap"])
+    def build():
+        host = {name: view(hsum, name).numpy() for name, _, _ in sections}
+        choice = host["choice"].reshape(G, nT).astype(np.int64)
+        if (choice < 0).any():
+            raise ProfilerError("no feasible policy met the threshold")
+        return ProfileResult(
+            family=family, thresholds=thresholds, recovery=host["recovery"].reshape(G, F),
+            cost=host["cost"].reshape(G, F).astype(np.int64), cosine=host["cosine"].reshape(G, F),
+            choice=choice, kept_count=host["kept_count"].astype(np.int64),
+            last_row_recovery=host["lrr"], topk_gap=host["gap"])
+
+    res = build() if pool is None else _PendingProfile(build, summary_ready)
     cache.profile_result = res
     cache._dargs = _decode_args(cache, dt)
     cache.track_recovery = bool(diagnostics)

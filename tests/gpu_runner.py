@@ -32,7 +32,7 @@ def torch_dtype(w):
 
 
 def run_arrays(q, k, v, cls, N, D, slopes, sinks, cfg=None, fixed=None, extra=(),
-               dtype=torch.float32, record_steps=True):
+               dtype=torch.float32, record_steps=True, pool=None):
     """q,k,v numpy float [B,H,T,d] (values exactly representable in dtype),
     cls uint8 [B,T].  Returns a dict in the golden layout."""
     dev = torch.device("cuda")
@@ -45,7 +45,7 @@ def run_arrays(q, k, v, cls, N, D, slopes, sinks, cfg=None, fixed=None, extra=()
     sk = None if sinks is None else torch.tensor(sinks, dtype=torch.float32, device=dev)
     res, cache = encode_prompt_tensors(qt, kt, vt, ct, cfg, fixed, prompt_len=N,
                                        max_new_tokens=D, extra_thresholds=extra, slopes=sl,
-                                       sinks=sk, diagnostics=True)
+                                       sinks=sk, diagnostics=True, pool=pool)
     G = B * H
     out = dict(res=res, cache=cache)
     enc_kept = np.zeros((G, N), bool)
@@ -77,7 +77,7 @@ def run_arrays(q, k, v, cls, N, D, slopes, sinks, cfg=None, fixed=None, extra=()
     return out
 
 
-def run_case(name):
+def run_case(name, pool=None):
     """CUDA path on a workload golden case, heads in golden order."""
     w, opts = C.case_workload(name)
     heads = C.case_heads(w, opts)
@@ -100,4 +100,4 @@ def run_case(name):
     else:
         cfg, fixed, extra = case_config(w, opts, dec_T), None, tuple(w.thresholds)
     return run_arrays(q, k, v, cls, w.N, w.D, w.slopes[hs], w.sinks[hs], cfg, fixed, extra,
-                      torch_dtype(w))
+                      torch_dtype(w), pool=pool)
