@@ -1237,14 +1237,14 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
 
 // ===========================================================================
 static int g_num_sms = 0;
-// CTAs per SM of the persistent decode grid (AKV_K3_CTAS_PER_SM, default 2)
-static int k3_ctas_per_sm() {
-  static int v = 0;
-  if (!v) {
-    const char* s = getenv("AKV_K3_CTAS_PER_SM");
-    v = (s && s[0] >= '1' && s[0] <= '4') ? s[0] - '0' : 2;
+// Decode grid: AKV_K3_GRID CTAs if set (tuning), else 2 per SM
+static int k3_grid(int sms) {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("AKV_K3_GRID");
+    v = s ? atoi(s) : 0;
   }
-  return v;
+  return v > 0 ? v : 2 * sms;
 }
 unsigned long long* g_dec_trace = nullptr;  // set by akv_debug_set_decode_trace
 
@@ -1292,7 +1292,7 @@ static cudaError_t launch_simt(const DecParams& p, cudaStream_t st) {
   int sms;
   if ((e = num_sms(&sms))) return e;
   const size_t smem = (size_t)kStages * S::STAGE_B + (size_t)(2 * p.G + 1) * 4;
-  return launch_pdl(kern, k3_ctas_per_sm() * sms, S::NW * 32 + 32, smem, st, p);
+  return launch_pdl(kern, k3_grid(sms), S::NW * 32 + 32, smem, st, p);
 }
 
 // tensor maps of the arena, cached per (base, slots) so steady-state steps
@@ -1341,7 +1341,7 @@ static cudaError_t launch_mma(const DecParams& p, int64_t total_slots, cudaStrea
   int sms;
   if ((e = num_sms(&sms))) return e;
   const size_t smem = 1024 + (size_t)kStages * S::STAGE_B + (size_t)(2 * p.G + 1) * 4 + p.G;
-  return launch_pdl(kern, k3_ctas_per_sm() * sms, S::THREADS, smem, st, p, tm->k, tm->v);
+  return launch_pdl(kern, k3_grid(sms), S::THREADS, smem, st, p, tm->k, tm->v);
 }
 
 struct DecWs {
