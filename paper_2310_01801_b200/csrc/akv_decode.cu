@@ -87,7 +87,7 @@ struct DecParams {
   int32_t* counter;  // [G]
   int max_parts;
   float scale;
-  unsigned long long* trace;  // optional [grid, 8] globaltimer stamps (AKV_DEC_TRACE)
+  unsigned long long* trace;  // optional [grid, 16] globaltimer stamps (debug hook)
   const int32_t* pos_dev;     // device position (CUDA-graph replays), overrides pos
   int flags;                  // AKV_DECODE_* flags
   float* lse_out;             // [G] log-sum-exp of each head's attended logits, or NULL
@@ -95,6 +95,7 @@ struct DecParams {
   int n_peers;
   int64_t peer_ld, peer_col0;
   int peer_bf16;
+  int l2_prefetch;            // pages prefetched into L2 ahead of the shared-memory ring
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -104,7 +105,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define AKV_TRACE(slot)                                                        \
   do {                                                                          \
-    if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 8 + (slot)] = gtimer(); \
+    if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 16 + (slot)] = gtimer(); \
   } while (0)
 
 // owner CTA of flattened page pg when P pages are split evenly over `grid`
@@ -447,7 +448,7 @@ __device__ void policy_v3(const DecParams& p, const HeadCtx& hc, float lse, int*
       }
     }
     if (mode == 2) {  // exact radix select over all candidates
-      if (p.trace && tid == 0) atomicAdd(&p.trace[blockIdx.x * 8 + 7], 1ull);
+      if (p.trace && tid == 0) atomicAdd(&p.trace[blockIdx.x * 16 + 7], 1ull);
       unsigned long long thr_key;
       int thr_pos;
       auto get = [&](int i, unsigned long long* key, int* pos) {
@@ -554,7 +555,7 @@ __device__ void policy_v3(const DecParams& p, const HeadCtx& hc, float lse, int*
 
 // ---------------------------------------------------------------------------
 // Epilogue of one head (consumer warps only, named barrier 1).
-template <typename CS, int D>
+template <typename CS, int D, bool kPolicy = true>
 __device__ void head_epilogue(const DecParams& p, const HeadCtx& hc, int nparts, int rv,
                               int* hist, int* red_i) {
   constexpr int NC = CS::kThreads, NW = CS::kWarps;
@@ -637,14 +638,14 @@ __device__ void head_epilogue(const DecParams& p, const HeadCtx& hc, int nparts,
     return;
   }
   const float lse = gM + logf(gl);
-  policy_v3<CS>(p, hc, lse, hist, red_i, rv);
+  if constexpr (kPolicy) policy_v3<CS>(p, hc, lse, hist, red_i, rv);
 }
 
 // Publish a CTA's partial (max, sum, o[D]) for head g from NWC per-warp
 // values in s_red / s_ml (group CS), bump the semaphore, and run the
 // epilogue if this CTA is the last contributor.  `release` (optional) is
 // arrived on once s_red / s_ml have been consumed.
-template <typename CS, int NWC, int D>
+template <typename CS, int NWC, int D, bool kPolicy = true>
 __device__ __forceinline__ void publish_head(const DecParams& p, const HeadCtx& hc,
                                              const int* s_prefix, long long P, int grid,
                                              const float (*s_red)[D], const float (*s_ml)[2],
@@ -654,6 +655,7 @@ __device__ __forceinline__ void publish_head(const DecParams& p, const HeadCtx& 
   const int tid = CS::tid();
   const int g = hc.g;
   CS::sync();
+  if (p.trace && tid == 0) p.trace[blockIdx.x * 16 + 8] = gtimer();   // publish start
   const int own0 = page_owner(s_prefix[g], P, grid);
   const int nparts = page_owner(s_prefix[g + 1] - 1, P, grid) - own0 + 1;
   float* part = p.part + ((size_t)g * p.max_parts + (blockIdx.x - own0)) * (D + 2);
@@ -682,9 +684,11 @@ __device__ __forceinline__ void publish_head(const DecParams& p, const HeadCtx& 
     asm volatile("fence.acq_rel.gpu;\n\tatom.add.acq_rel.gpu.global.s32 %0, [%1], 1;"
                  : "=r"(prev) : "l"(p.counter + g) : "memory");
     *s_last = (prev == nparts - 1);
+    if (p.trace) p.trace[blockIdx.x * 16 + 9] = gtimer();                // partial released
   }
   CS::sync();
-  if (*s_last) head_epilogue<CS, D>(p, hc, nparts, rv, hist, red_i);
+  if (*s_last) head_epilogue<CS, D, kPolicy>(p, hc, nparts, rv, hist, red_i);
+  if (p.trace && tid == 0) p.trace[blockIdx.x * 16 + 10] = gtimer();    // segment finished
 }
 
 // ===========================================================================
@@ -1002,7 +1006,24 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
       bool waited = !early;
       int g = g0, stage = 0, gl = -1, L = 0;
       uint32_t phase = 0;
+      // L2 prefetch cursor: the pages just beyond the shared-memory ring go
+      // to L2 early (coherent, so safe before the previous step drains),
+      // raising the bytes in flight per CTA beyond what the ring can hold
+      long long pf = pbeg + kStages;
+      int gpf = g0;
       for (long long pg = pbeg; pg < pend; ++pg) {
+        for (const long long lim = min(pend, pg + kStages + p.l2_prefetch); pf < lim; ++pf) {
+          while (pf >= s_prefix[gpf + 1]) ++gpf;
+          const int s0 = (int)(pf - s_prefix[gpf]) * PAGE;
+          if (s0 <= s_live[gpf]) {
+            const int row0 = (int)(p.seg_off[gpf] + s0);
+#pragma unroll
+            for (int bx = 0; bx < S::NBOX; ++bx) {
+              tma_prefetch_l2_2d(&tmK, bx * 64, row0);
+              tma_prefetch_l2_2d(&tmV, bx * 64, row0);
+            }
+          }
+        }
         while (pg >= s_prefix[g + 1]) ++g;
         if (g != gl) {
           gl = g;
@@ -1058,18 +1079,21 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
     int pub_n = 0;
     for (int g = g0; g < G && s_prefix[g] < pend; ++g) {
       if (s_prefix[g + 1] == s_prefix[g]) continue;  // head without pages
+      // the consumers publish the CTA's last segment themselves when it
+      // belongs to a full-cache head (no policy to run)
+      if (s_prefix[g + 1] >= pend && (p.atoms[g] & AKV_ATOM_FULL)) break;
       const int slot = pub_n & 1;
       mbar_wait(&pub_full[slot], (pub_n >> 1) & 1);
       const HeadCtx hc = s_pub[slot].ctx;
       publish_head<ES, NW, D>(p, hc, s_prefix, P, grid, s_pub[slot].red, s_pub[slot].ml, &s_last,
                               RB / 16, hist, red_i, &pub_empty[slot]);
       if (s_last && p.trace && ES::tid() == 0) {
-        atomicAdd(&p.trace[blockIdx.x * 8 + 5], 1ull);               // epilogues run
-        if (hc.freq) atomicAdd(&p.trace[blockIdx.x * 8 + 6], 1ull);  // frequent ones
+        atomicAdd(&p.trace[blockIdx.x * 16 + 5], 1ull);               // epilogues run
+        if (hc.freq) atomicAdd(&p.trace[blockIdx.x * 16 + 6], 1ull);  // frequent ones
       }
       ++pub_n;
     }
-    if (p.trace && ES::tid() == 0) p.trace[blockIdx.x * 8 + 4] = gtimer();
+    if (p.trace && ES::tid() == 0) p.trace[blockIdx.x * 16 + 4] = gtimer();
     return;
   }
 
@@ -1205,8 +1229,31 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
     if (++stage == kStages) { stage = 0; phase ^= 1; }
 
     if (!((pg + 1 == pend) || (pg + 1 == s_prefix[g + 1]))) continue;
-    // hand the segment to the epilogue warps and keep streaming
     l_run = warp_allreduce(l_run, [](float a, float b) { return a + b; });
+    if (pg + 1 == pend && (hc.atoms & AKV_ATOM_FULL)) {
+      // The CTA's last segment, of a full-cache head: publish it from the
+      // consumer warps, in parallel with the epilogue warps finishing the
+      // previous segment (that serialisation was the step's tail).  Every
+      // page has been consumed, so stage 0 holds the handoff scratch.
+      using CSync = NamedSync<NW * 32, 3, 0>;
+      CSync::sync();  // all consumer warps are past the last page
+      float(*red)[D] = reinterpret_cast<float(*)[D]>(smem);
+      float(*mls)[2] = reinterpret_cast<float(*)[2]>(smem + NW * D * 4);
+      int* scratch_i = reinterpret_cast<int*>(smem + NW * D * 4 + 64);
+      if (qq == 0) {
+#pragma unroll
+        for (int tt = 0; tt < NK; ++tt) {
+          red[warp][tt * 16 + gq] = o[tt][0];
+          red[warp][tt * 16 + gq + 8] = o[tt][2];
+        }
+      }
+      if (lane == 0) { mls[warp][0] = m_run; mls[warp][1] = l_run; }
+      AKV_TRACE(3);
+      publish_head<CSync, NW, D, false>(p, hc, s_prefix, P, grid, red, mls, scratch_i + 300,
+                                        RB / 16, scratch_i, scratch_i + 256, nullptr);
+      return;
+    }
+    // hand the segment to the epilogue warps and keep streaming
     {
       const int slot = pub_n & 1;
       mbar_wait(&pub_empty[slot], ((pub_n >> 1) & 1) ^ 1);
@@ -1247,6 +1294,16 @@ static int k3_grid(int sms) {
   return v > 0 ? v : 2 * sms;
 }
 unsigned long long* g_dec_trace = nullptr;  // set by akv_debug_set_decode_trace
+// pages of L2 prefetch ahead of the ring (AKV_K3_L2_PREFETCH, tuning)
+static int k3_l2_prefetch() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("AKV_K3_L2_PREFETCH");
+    v = s ? atoi(s) : 0;  // measured at config 1: 0 best (2: +0.6 us, 4: +1.4, 8: +4.1)
+    if (v < 0) v = 0;
+  }
+  return v;
+}
 
 static cudaError_t num_sms(int* out) {
   if (!g_num_sms) {
@@ -1380,7 +1437,7 @@ static DecWs carve(void* ws, int B, int H, int d, int max_cap, int64_t total_slo
 using namespace akv;
 
 // Debug hook (not part of the ABI header): record per-CTA timestamps of
-// the next decode launches into a device buffer of [2*SMs, 8] uint64.
+// the next decode launches into a device buffer of [2*SMs, 16] uint64.
 extern "C" void akv_debug_set_decode_trace(void* buf) {
   g_dec_trace = static_cast<unsigned long long*>(buf);
 }
@@ -1427,7 +1484,7 @@ extern "C" int akv_decode_step(const akv_decode_args* a, void* stream) {
               a->evicted_dev, a->status_dev ? a->status_dev : w.status, w.part, w.logit, w.counter,
               w.max_parts, (float)(1.0 / sqrt((double)a->d)), g_dec_trace, a->pos_dev, a->flags,
               a->lse_out_dev, a->peer_out_dev, a->n_peers, a->peer_ld, a->peer_col0,
-              a->dtype == AKV_DTYPE_BF16};
+              a->dtype == AKV_DTYPE_BF16, k3_l2_prefetch()};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaErrorInvalidValue;
   bool ok = true;

@@ -31,7 +31,7 @@ def main():
     _, c = encode_prompt_tensors(qd, kd, vd, cd, ProfilerConfig(recovery_threshold=T), prompt_len=N,
                                  max_new_tokens=D, slopes=sl, sinks=sk)
     sms = torch.cuda.get_device_properties(0).multi_processor_count
-    bufs = [torch.zeros(2 * sms * 8, dtype=torch.int64, device=dev) for _ in range(K)]
+    bufs = [torch.zeros(2 * sms * 16, dtype=torch.int64, device=dev) for _ in range(K)]
     lib.akv_debug_set_decode_trace.argtypes = [ctypes.c_void_p]
     for t in range(at + K):
         if at <= t < at + K:
@@ -39,7 +39,7 @@ def main():
         decode_step_tensors(c, qd[:, :, N + t], kd[:, :, N + t], vd[:, :, N + t], cls[t], chained=True)
         lib.akv_debug_set_decode_trace(None)
     torch.cuda.synchronize()
-    trs = [b.view(-1, 8).cpu().numpy().astype(np.float64) for b in bufs]
+    trs = [b.view(-1, 16).cpu().numpy().astype(np.float64) for b in bufs]
     t0 = min(tr[tr[:, 4] > 0, 0].min() for tr in trs)
     for k, tr in enumerate(trs):
         ok = tr[:, 4] > 0

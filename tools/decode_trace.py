@@ -29,7 +29,7 @@ def main():
     _, c = encode_prompt_tensors(qd, kd, vd, cd, ProfilerConfig(recovery_threshold=T), prompt_len=N,
                                  max_new_tokens=D, slopes=sl, sinks=sk)
     sms = torch.cuda.get_device_properties(0).multi_processor_count
-    buf = torch.zeros(2 * sms * 8, dtype=torch.int64, device=dev)
+    buf = torch.zeros(2 * sms * 16, dtype=torch.int64, device=dev)
     lib.akv_debug_set_decode_trace.argtypes = [ctypes.c_void_p]
     for t in range(max(ats) + 1):
         if t in ats:
@@ -45,7 +45,7 @@ def main():
 
 
 def report(buf, T, at, verbose):
-    tr = buf.view(-1, 8).cpu().numpy().astype(np.float64)
+    tr = buf.view(-1, 16).cpu().numpy().astype(np.float64)
     ok = tr[:, 4] > 0
     t0 = tr[ok, 0].min()
     rel = (tr[ok, :5] - t0) / 1e3
@@ -60,9 +60,17 @@ def report(buf, T, at, verbose):
     ep = tr[ok, 5]
     fq = tr[ok, 6]
     print(f"  epilogues per CTA: {np.bincount(ep.astype(int)).tolist()}, frequent: {int(fq.sum())}, top-k fallbacks: {int(tr[ok, 7].sum())}")
+    ph = (tr[ok][:, 8:11] - t0) / 1e3  # last segment: publish start, partial released, finished
+    print(f"  last segment: publish start p50 {np.median(ph[:, 0]):.1f}, released p50 "
+          f"{np.median(ph[:, 1]):.1f}, finished p50 {np.median(ph[:, 2]):.1f}; "
+          f"last page -> publish start p50 {np.median(ph[:, 0] - rel[:, 3]):.1f} us, "
+          f"publish -> released p50 {np.median(ph[:, 1] - ph[:, 0]):.1f} us, "
+          f"released -> finished p50 {np.median(ph[:, 2] - ph[:, 1]):.1f} us")
     late = np.argsort(-rel[:, 4])[:5]
     for i in late:
-        print(f"  late CTA: planned {rel[i,1]:.1f} first {rel[i,2]:.1f} last {rel[i,3]:.1f} done {rel[i,4]:.1f} ep {int(ep[i])} freq {int(fq[i])}")
+        print(f"  late CTA: planned {rel[i,1]:.1f} first {rel[i,2]:.1f} last {rel[i,3]:.1f} "
+              f"publish {ph[i,0]:.1f} released {ph[i,1]:.1f} finished {ph[i,2]:.1f} "
+              f"done {rel[i,4]:.1f} ep {int(ep[i])} freq {int(fq[i])}")
 
 
 if __name__ == "__main__":
