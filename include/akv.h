@@ -260,6 +260,8 @@ typedef struct akv_diag_args {
   uint8_t* cls_hist_dev;         /* [B, cls_ld] class of every position (in/out), or NULL */
   int64_t cls_ld;
   double* recovery_dev;          /* [B*H] out */
+  const uint8_t* head_atoms_dev; /* optional [B*H] policy atoms (akv_compact): full-cache heads
+                                    report 1 exactly and skip the shadow stream */
   void* workspace_dev;           /* akv_decode_recovery_workspace_size bytes, initialised once */
   size_t workspace_bytes;
 } akv_diag_args;

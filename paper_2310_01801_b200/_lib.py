@@ -94,7 +94,7 @@ class DiagArgs(C.Structure):
         ("q_dev", P), ("k_dev", P), ("bh_stride", i64), ("new_cls_dev", P), ("slope_dev", P),
         ("sink_dev", P), ("seg_off_dev", P), ("live_in_dev", P), ("meta_dev", P),
         ("shadow_dev", P), ("shadow_ld", i64), ("cls_hist_dev", P), ("cls_ld", i64),
-        ("recovery_dev", P), ("workspace_dev", P), ("workspace_bytes", sz),
+        ("recovery_dev", P), ("head_atoms_dev", P), ("workspace_dev", P), ("workspace_bytes", sz),
     ]
 
 

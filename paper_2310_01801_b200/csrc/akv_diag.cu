@@ -28,7 +28,7 @@
 namespace akv {
 
 constexpr int kDiagThreads = 256;
-constexpr int kChunk = 512;  // positions per CTA
+constexpr int kChunk = 128;  // positions per CTA
 
 struct DiagWs {
   float4* part;     // [G, max_chunks] (max, total mass, attended mass, -)
@@ -86,6 +86,12 @@ __global__ void __launch_bounds__(kDiagThreads, 4) k_decode_recovery(akv_diag_ar
   static_assert(LPR >= 1 && LPR <= 32 && 32 % LPR == 0, "head dim");
   const int g = blockIdx.y, chunk = blockIdx.x;
   const int b = g / a.H, h = g % a.H;
+  // a full-cache head attends to every position: its recovery is exactly 1
+  // and its shadow keys are never needed (policies are frozen per session)
+  if (a.head_atoms_dev && (a.head_atoms_dev[g] & AKV_ATOM_FULL)) {
+    if (chunk == 0 && threadIdx.x == 0) a.recovery_dev[g] = 1.0;
+    return;
+  }
   const int pos = a.pos_dev ? *a.pos_dev : a.pos;
   const int n = pos + 1;
   const int nchunks = (n + kChunk - 1) / kChunk;

@@ -528,6 +528,7 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
         g.shadow_dev, g.shadow_ld = _ptr(cache.shadow), shadow_ld
         g.cls_hist_dev, g.cls_ld = _ptr(cache.cls_hist), cache.cls_hist.shape[1]
         g.recovery_dev = _ptr(cache.step_recovery)
+        g.head_atoms_dev = _ptr(cache.head_atoms)
         g.workspace_dev, g.workspace_bytes = _ptr(cache.diag_ws), ws
         cache._diag_args = g
     return res, cache
