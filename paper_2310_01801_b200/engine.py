@@ -12,27 +12,27 @@ functions are built on: q, k, v are device tensors ``[B, H, ld, d]``
 
 The host only orchestrates: it allocates device memory (PyTorch is used
 for allocation and streams), reads back the per-head profile once after
-K1 (one small device->host copy that also sizes the ragged arena), and
-launches kernels.  There is no CPU compute path.
+K1 (one small device->host copy that also sizes the ragged arena - or, with
+an ``ArenaPool``, no synchronous read at all), and launches kernels.  There
+is no CPU compute path.
 """
 
 from __future__ import annotations
 
 import ctypes as C
 import json
-import math
 from dataclasses import dataclass, field
 
 import numpy as np
 import torch
 
 from . import _lib
-from ._lib import (ATOM_FULL, CRIT_COSINE, CRIT_RECOVERY, DTYPE_BF16, DTYPE_F32, ROWS_ALL,
-                   ROWS_LAST, CompactArgs, DecodeArgs, ProfileArgs, check, lib)
-from .policies import CompressionPolicy, PolicyAtom, full_policy
+from ._lib import (CRIT_COSINE, CRIT_RECOVERY, DTYPE_BF16, DTYPE_F32, ROWS_ALL, ROWS_LAST,
+                   CompactArgs, DecodeArgs, ProfileArgs, check, lib)
+from .policies import CompressionPolicy, full_policy
 from .profiler import (HeadDecision, HeadProfile, ProfilerConfig, ProfilerError, RowAveraging,
                        SelectionCriterion)
-from .tokens import CLASS_CODE, TokenAnnotation, VocabMetadata, classify_tokens
+from .tokens import CLASS_CODE, TokenAnnotation, classify_tokens
 
 
 class EngineError(ValueError):
