@@ -452,19 +452,42 @@ __global__ void __launch_bounds__(kTcThreads, 2)
       s_lastp[kl] = lastp;
     }
     EpiSync::sync();
-    if (half == 0) {
-      // last-row output partial of this key tile: sum_j lastp_j V_j (d = 128 = one dim per thread)
+    {
+      // last-row output partial of this key tile, sum_j lastp_j V_j, by all
+      // epilogue threads: 16-byte loads of 8 dims, every load in flight at
+      // once (a per-dimension loop here was a chain of ~30 L2/DRAM round
+      // trips at the end of every CTA); partials meet in the drained rings
+      static_assert(kTT * 128 / 8 == 8 * 32 * kEpiWarps, "16-byte loads per epilogue thread");
+      constexpr int RG = 32 * kEpiWarps / 16;  // row groups
       const __nv_bfloat16* vt = p.v + ((size_t)g * p.ld + (size_t)kt * kTT) * 128;
       const int nrow = min(kTT, p.N - kt * kTT);
-      float o[4] = {0.f, 0.f, 0.f, 0.f};
-      int j = 0;
-      for (; j + 4 <= nrow; j += 4) {
+      const int c = et & 15, r0 = et >> 4;
+      uint4 raw[kTT / RG];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          o[u] = fmaf(s_lastp[j + u], __bfloat162float(vt[(size_t)(j + u) * 128 + et]), o[u]);
+      for (int k = 0; k < kTT / RG; ++k) {
+        const int j = r0 + RG * k;
+        raw[k] = j < nrow ? ld_nc_v4(vt + (size_t)j * 128 + c * 8) : make_uint4(0u, 0u, 0u, 0u);
       }
-      for (; j < nrow; ++j) o[0] = fmaf(s_lastp[j], __bfloat162float(vt[(size_t)j * 128 + et]), o[0]);
-      p.out_part[((size_t)g * ntiles + kt) * 128 + et] = (o[0] + o[1]) + (o[2] + o[3]);
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int k = 0; k < kTT / RG; ++k) {
+        const int j = r0 + RG * k;
+        const float w = j < nrow ? s_lastp[j] : 0.f;
+        float f[8];
+        Elem<__nv_bfloat16>::unpack(raw[k], f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = fmaf(w, f[e], acc[e]);
+      }
+      float* red = reinterpret_cast<float*>(smem);  // [RG][128]; all TMA / MMA work is done
+#pragma unroll
+      for (int e = 0; e < 8; ++e) red[r0 * 128 + c * 8 + e] = acc[e];
+      EpiSync::sync();
+      if (half == 0) {
+        float o = 0.f;
+#pragma unroll
+        for (int r = 0; r < RG; ++r) o += red[r * 128 + et];
+        p.out_part[((size_t)g * ntiles + kt) * 128 + et] = o;
+      }
     }
   }
   tc_fence_before();
