@@ -124,7 +124,12 @@ __device__ __forceinline__ void row_update_raw(const float* v, float sl2, float&
   m = mn;
 }
 
-// ---------------------------------------------------------------------------
+// Work pairing: CTA (x, g) processes query tiles x and ntiles-1-x of head g
+// (one when they coincide), so every CTA carries ntiles+1 key tiles of the
+// triangle - uniform work, half the CTA setups.  TMEM, the barriers and the
+// tensor-map prefetch serve both items, the second item's Q tile loads as
+// soon as the first item's last MMA has read sQ, and all ring / accumulator
+// phases run on per-CTA counters.
 __global__ void __launch_bounds__(kTcThreads, 2)
     k1tc_rowlse(const __grid_constant__ TcParams p, const __grid_constant__ CUtensorMap tmQ,
                 const __grid_constant__ CUtensorMap tmK) {
@@ -132,16 +137,19 @@ __global__ void __launch_bounds__(kTcThreads, 2)
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sQ = smem;
   uint8_t* sK = smem + kTileB;
-  __shared__ __align__(8) uint64_t q_full, k_full[kRing], k_empty[kRing], acc_full[2], acc_empty[2];
+  __shared__ __align__(8) uint64_t q_full, q_empty, k_full[kRing], k_empty[kRing], acc_full[2],
+      acc_empty[2];
   __shared__ uint32_t s_tmem;
   __shared__ __align__(16) float s_col[2][kTT];
   const int ntiles = (p.N + kTT - 1) / kTT;
   const int g = blockIdx.y, h = g % p.H, b = g / p.H;
-  const int qt = ntiles - 1 - blockIdx.x;  // heaviest (most key tiles) first
-  const int nk = qt + 1;
+  const int x = blockIdx.x;
+  const int nitems = (ntiles - 1 - x == x) ? 1 : 2;
+  auto item_qt = [&](int j) { return j == 0 ? ntiles - 1 - x : x; };  // heavier first
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     mbar_init(&q_full, 1);
+    mbar_init(&q_empty, 1);
     for (int s = 0; s < kRing; ++s) { mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&acc_full[a], 1); mbar_init(&acc_empty[a], kEpiWarps); }
     mbar_fence_init();
@@ -157,109 +165,125 @@ __global__ void __launch_bounds__(kTcThreads, 2)
   if (warp == 0) {  // ---------------- TMA producer ----------------
     if (lane == 0) {
       const uint64_t pol_q = policy_evict_first(), pol_k = policy_evict_last();
-      const int rq = (int)((int64_t)g * p.ld + (int64_t)qt * kTT);
-      mbar_arrive_expect_tx(&q_full, kTileB);
-      tma_load_2d(sQ, &tmQ, 0, rq, &q_full, pol_q);
-      tma_load_2d(sQ + kBoxB, &tmQ, 64, rq, &q_full, pol_q);
-      for (int kt = 0; kt < nk; ++kt) {
-        const int s = kt % kRing;
-        mbar_wait(&k_empty[s], ((kt / kRing) & 1) ^ 1);
-        mbar_arrive_expect_tx(&k_full[s], kTileB);
-        const int rk = (int)((int64_t)g * p.ld + (int64_t)kt * kTT);
-        tma_load_2d(sK + s * kTileB, &tmK, 0, rk, &k_full[s], pol_k);
-        tma_load_2d(sK + s * kTileB + kBoxB, &tmK, 64, rk, &k_full[s], pol_k);
+      int t = 0;
+      for (int j = 0; j < nitems; ++j) {
+        const int qt = item_qt(j);
+        const int rq = (int)((int64_t)g * p.ld + (int64_t)qt * kTT);
+        mbar_wait(&q_empty, (j & 1) ^ 1);  // the previous item's MMAs have read sQ
+        mbar_arrive_expect_tx(&q_full, kTileB);
+        tma_load_2d(sQ, &tmQ, 0, rq, &q_full, pol_q);
+        tma_load_2d(sQ + kBoxB, &tmQ, 64, rq, &q_full, pol_q);
+        for (int kt = 0; kt <= qt; ++kt, ++t) {
+          const int s = t % kRing;
+          mbar_wait(&k_empty[s], ((t / kRing) & 1) ^ 1);
+          mbar_arrive_expect_tx(&k_full[s], kTileB);
+          const int rk = (int)((int64_t)g * p.ld + (int64_t)kt * kTT);
+          tma_load_2d(sK + s * kTileB, &tmK, 0, rk, &k_full[s], pol_k);
+          tma_load_2d(sK + s * kTileB + kBoxB, &tmK, 64, rk, &k_full[s], pol_k);
+        }
       }
     }
   } else if (warp == 1) {  // ---------------- MMA issuer ----------------
     if (lane == 0) {
-      mbar_wait(&q_full, 0);
-      for (int kt = 0; kt < nk; ++kt) {
-        const int s = kt % kRing, a = kt & 1;
-        mbar_wait(&k_full[s], (kt / kRing) & 1);
-        mbar_wait(&acc_empty[a], ((kt >> 1) & 1) ^ 1);
-        tc_fence_after();
-        mma_tile(tmem + a * kTT, sQ, sK + s * kTileB);
-        umma_commit(&k_empty[s]);
-        umma_commit(&acc_full[a]);
+      int t = 0;
+      for (int j = 0; j < nitems; ++j) {
+        const int qt = item_qt(j);
+        mbar_wait(&q_full, j & 1);
+        for (int kt = 0; kt <= qt; ++kt, ++t) {
+          const int s = t % kRing, a = t & 1;
+          mbar_wait(&k_full[s], (t / kRing) & 1);
+          mbar_wait(&acc_empty[a], ((t >> 1) & 1) ^ 1);
+          tc_fence_after();
+          mma_tile(tmem + a * kTT, sQ, sK + s * kTileB);
+          umma_commit(&k_empty[s]);
+          umma_commit(&acc_full[a]);
+        }
+        umma_commit(&q_empty);
       }
     }
   } else {  // ---------------- epilogue (warps 2-9) ----------------
-    __shared__ float s_ml[kGroups][kTT][2];
+    __shared__ float s_ml[2][kGroups][kTT][2];
     const int quarter = warp & 3;
     const int et = threadIdx.x - 64;
     const int half = et >> 7;  // column group: accumulator columns [kCols*half, kCols*(half+1))
     const int rl = quarter * 32 + lane;
-    const int row = qt * kTT + rl;
     const float sl2 = p.scale * kLog2e;
     const float slope_l2 = (p.slope ? p.slope[h] : 0.f) * kLog2e;
     const float sink_l2 = (p.sink ? p.sink[h] : 0.f) * kLog2e;
     const bool bias = slope_l2 != 0.f || sink_l2 != 0.f;
     const uint8_t* cls = p.cls + (size_t)b * p.cls_ld;
-    // logits in the log2 domain without the row term -slope*row, which is
-    // constant along a row and joins the lse at the end
-    float m = -INFINITY, l = 0.f;
-    uint8_t cnext = 0;
-    if (bias && et < kTT) cnext = et < p.N ? cls[et] : 0;
-    for (int kt = 0; kt < nk; ++kt) {
-      const int a = kt & 1;
-      if (bias) {  // per-column bias of this key tile: sink on special keys + slope * col
-        if (et < kTT) {
-          const int col = kt * kTT + et;
-          s_col[a][et] = (cnext == AKV_CLS_SPECIAL ? sink_l2 : 0.f) + slope_l2 * (float)col;
-          const int nc = col + kTT;
-          cnext = (kt + 1 < nk && nc < p.N) ? cls[nc] : 0;
+    int t = 0;
+    for (int j = 0; j < nitems; ++j) {
+      const int qt = item_qt(j);
+      const int nk = qt + 1;
+      const int row = qt * kTT + rl;
+      // logits in the log2 domain without the row term -slope*row, which is
+      // constant along a row and joins the lse at the end
+      float m = -INFINITY, l = 0.f;
+      uint8_t cnext = 0;
+      if (bias && et < kTT) cnext = et < p.N ? cls[et] : 0;
+      for (int kt = 0; kt < nk; ++kt, ++t) {
+        const int a = t & 1;
+        if (bias) {  // per-column bias of this key tile: sink on special keys + slope * col
+          if (et < kTT) {
+            const int col = kt * kTT + et;
+            s_col[a][et] = (cnext == AKV_CLS_SPECIAL ? sink_l2 : 0.f) + slope_l2 * (float)col;
+            const int nc = col + kTT;
+            cnext = (kt + 1 < nk && nc < p.N) ? cls[nc] : 0;
+          }
+          EpiSync::sync();
         }
-        EpiSync::sync();
-      }
-      mbar_wait(&acc_full[a], (kt >> 1) & 1);
-      tc_fence_after();
-      float v[kCols];
-      tmem_ld_cols(tmem + ((uint32_t)(quarter * 32) << 16) + a * kTT + half * kCols, v);
-      // the values are in registers: hand the accumulator back to the MMA warp
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[a]);
-      const bool masked = (kt == qt) || ((kt + 1) * kTT > p.N);
-      const float* ct = &s_col[a][half * kCols];
-      if (masked) {  // diagonal / ragged tile: causal and length masks
-        const int c0 = kt * kTT + half * kCols;
+        mbar_wait(&acc_full[a], (t >> 1) & 1);
+        tc_fence_after();
+        float v[kCols];
+        tmem_ld_cols(tmem + ((uint32_t)(quarter * 32) << 16) + a * kTT + half * kCols, v);
+        // the values are in registers: hand the accumulator back to the MMA warp
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[a]);
+        const bool masked = (kt == qt) || ((kt + 1) * kTT > p.N);
+        const float* ct = &s_col[a][half * kCols];
+        if (masked) {  // diagonal / ragged tile: causal and length masks
+          const int c0 = kt * kTT + half * kCols;
 #pragma unroll
-        for (int c = 0; c < kCols; ++c) {
-          float y = bias ? fmaf(v[c], sl2, ct[c]) : v[c] * sl2;
-          if (c0 + c > row || c0 + c >= p.N) y = -INFINITY;
-          v[c] = y;
+          for (int c = 0; c < kCols; ++c) {
+            float y = bias ? fmaf(v[c], sl2, ct[c]) : v[c] * sl2;
+            if (c0 + c > row || c0 + c >= p.N) y = -INFINITY;
+            v[c] = y;
+          }
+          row_update_scaled(v, m, l);
+        } else if (bias) {
+#pragma unroll
+          for (int c = 0; c < kCols; c += 4) {
+            const float4 tt = *reinterpret_cast<const float4*>(ct + c);
+            v[c] = fmaf(v[c], sl2, tt.x);
+            v[c + 1] = fmaf(v[c + 1], sl2, tt.y);
+            v[c + 2] = fmaf(v[c + 2], sl2, tt.z);
+            v[c + 3] = fmaf(v[c + 3], sl2, tt.w);
+          }
+          row_update_scaled(v, m, l);
+        } else {
+          row_update_raw(v, sl2, m, l);
         }
-        row_update_scaled(v, m, l);
-      } else if (bias) {
+      }
+      // merge the column groups of every row (double-buffered by item)
+      float(*ml)[kTT][2] = s_ml[j & 1];
+      ml[half][rl][0] = m;
+      ml[half][rl][1] = l;
+      EpiSync::sync();
+      if (half == 0) {
+        float mm = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < kCols; c += 4) {
-          const float4 t = *reinterpret_cast<const float4*>(ct + c);
-          v[c] = fmaf(v[c], sl2, t.x);
-          v[c + 1] = fmaf(v[c + 1], sl2, t.y);
-          v[c + 2] = fmaf(v[c + 2], sl2, t.z);
-          v[c + 3] = fmaf(v[c + 3], sl2, t.w);
+        for (int gq = 0; gq < kGroups; ++gq) mm = fmaxf(mm, ml[gq][rl][0]);
+        float ll = 0.f;
+#pragma unroll
+        for (int gq = 0; gq < kGroups; ++gq) {
+          const float m2 = ml[gq][rl][0];
+          if (m2 != -INFINITY) ll += ml[gq][rl][1] * fast_exp2(m2 - mm);
         }
-        row_update_scaled(v, m, l);
-      } else {
-        row_update_raw(v, sl2, m, l);
+        const float rowterm = -slope_l2 * (float)row;
+        if (row < p.N) p.lse[(size_t)g * p.N + row] = (mm + rowterm + __log2f(ll)) * kLn2;
       }
-    }
-    // merge the column groups of every row
-    s_ml[half][rl][0] = m;
-    s_ml[half][rl][1] = l;
-    EpiSync::sync();
-    if (half == 0) {
-      float mm = -INFINITY;
-#pragma unroll
-      for (int gq = 0; gq < kGroups; ++gq) mm = fmaxf(mm, s_ml[gq][rl][0]);
-      float ll = 0.f;
-#pragma unroll
-      for (int gq = 0; gq < kGroups; ++gq) {
-        const float m2 = s_ml[gq][rl][0];
-        if (m2 != -INFINITY) ll += s_ml[gq][rl][1] * fast_exp2(m2 - mm);
-      }
-      const float rowterm = -slope_l2 * (float)row;
-      if (row < p.N) p.lse[(size_t)g * p.N + row] = (mm + rowterm + __log2f(ll)) * kLn2;
     }
   }
   tc_fence_before();
@@ -525,7 +549,8 @@ cudaError_t launch_tc_passes(const void* q, const void* k, const void* v, int B,
   TcParams p{H, N, ld, cls, cls_ld, slope, sink, static_cast<const __nv_bfloat16*>(v), lse, colsum,
              colsq, lastp, out_part, (float)(1.0 / sqrt(128.0))};
   const dim3 grid(tc_tiles(N), G);
-  k1tc_rowlse<<<grid, kTcThreads, kTcSmem, st>>>(p, tmQ, tmK);
+  const dim3 pairs((tc_tiles(N) + 1) / 2, G);  // query tiles x and ntiles-1-x share a CTA
+  k1tc_rowlse<<<pairs, kTcThreads, kTcSmem, st>>>(p, tmQ, tmK);
   if ((e = cudaGetLastError())) return e;
   k1tc_colsum<<<grid, kTcThreads, kTcSmem, st>>>(p, tmQ, tmK);
   return cudaGetLastError();
