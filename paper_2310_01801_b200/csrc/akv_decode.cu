@@ -96,6 +96,7 @@ struct DecParams {
   int64_t peer_ld, peer_col0;
   int peer_bf16;
   int l2_prefetch;            // pages prefetched into L2 ahead of the shared-memory ring
+  int consumer_tail;          // consumers publish the CTA's last full-cache segment
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -1081,7 +1082,7 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
       if (s_prefix[g + 1] == s_prefix[g]) continue;  // head without pages
       // the consumers publish the CTA's last segment themselves when it
       // belongs to a full-cache head (no policy to run)
-      if (s_prefix[g + 1] >= pend && (p.atoms[g] & AKV_ATOM_FULL)) break;
+      if (p.consumer_tail && s_prefix[g + 1] >= pend && (p.atoms[g] & AKV_ATOM_FULL)) break;
       const int slot = pub_n & 1;
       mbar_wait(&pub_full[slot], (pub_n >> 1) & 1);
       const HeadCtx hc = s_pub[slot].ctx;
@@ -1230,7 +1231,7 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
 
     if (!((pg + 1 == pend) || (pg + 1 == s_prefix[g + 1]))) continue;
     l_run = warp_allreduce(l_run, [](float a, float b) { return a + b; });
-    if (pg + 1 == pend && (hc.atoms & AKV_ATOM_FULL)) {
+    if (p.consumer_tail && pg + 1 == pend && (hc.atoms & AKV_ATOM_FULL)) {
       // The CTA's last segment, of a full-cache head: publish it from the
       // consumer warps, in parallel with the epilogue warps finishing the
       // previous segment (that serialisation was the step's tail).  Every
@@ -1294,6 +1295,15 @@ static int k3_grid(int sms) {
   return v > 0 ? v : 2 * sms;
 }
 unsigned long long* g_dec_trace = nullptr;  // set by akv_debug_set_decode_trace
+// consumers publish the CTA's last full-cache segment (AKV_K3_CONSUMER_TAIL, tuning)
+static int k3_consumer_tail() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("AKV_K3_CONSUMER_TAIL");
+    v = s ? atoi(s) != 0 : 1;
+  }
+  return v;
+}
 // pages of L2 prefetch ahead of the ring (AKV_K3_L2_PREFETCH, tuning)
 static int k3_l2_prefetch() {
   static int v = -1;
@@ -1484,7 +1494,7 @@ extern "C" int akv_decode_step(const akv_decode_args* a, void* stream) {
               a->evicted_dev, a->status_dev ? a->status_dev : w.status, w.part, w.logit, w.counter,
               w.max_parts, (float)(1.0 / sqrt((double)a->d)), g_dec_trace, a->pos_dev, a->flags,
               a->lse_out_dev, a->peer_out_dev, a->n_peers, a->peer_ld, a->peer_col0,
-              a->dtype == AKV_DTYPE_BF16, k3_l2_prefetch()};
+              a->dtype == AKV_DTYPE_BF16, k3_l2_prefetch(), k3_consumer_tail()};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaErrorInvalidValue;
   bool ok = true;
