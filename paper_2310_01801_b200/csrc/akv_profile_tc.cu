@@ -145,6 +145,8 @@ __global__ void __launch_bounds__(kTcThreads, 2)
   const int g = blockIdx.y, h = g % p.H, b = g / p.H;
   const int x = blockIdx.x;
   const int nitems = (ntiles - 1 - x == x) ? 1 : 2;
+  // the column pass may launch now; it reads lse only after griddepcontrol.wait
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   auto item_qt = [&](int j) { return j == 0 ? ntiles - 1 - x : x; };  // heavier first
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -378,6 +380,9 @@ __global__ void __launch_bounds__(kTcThreads, 2)
     float lastp = 0.f;
     const int qlast = p.N - 1;
     float lnext = 0.f;
+    // the row pass (programmatic predecessor) must be complete before lse is
+    // read; the producer and MMA warps run ahead meanwhile
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (et < kTT) lnext = kt * kTT + et < p.N ? lse[kt * kTT + et] : 0.f;
     for (int i = 0; i < nq; ++i) {
       const int a = i & 1;
@@ -552,7 +557,20 @@ cudaError_t launch_tc_passes(const void* q, const void* k, const void* v, int B,
   const dim3 pairs((tc_tiles(N) + 1) / 2, G);  // query tiles x and ntiles-1-x share a CTA
   k1tc_rowlse<<<pairs, kTcThreads, kTcSmem, st>>>(p, tmQ, tmK);
   if ((e = cudaGetLastError())) return e;
-  k1tc_colsum<<<grid, kTcThreads, kTcSmem, st>>>(p, tmQ, tmK);
+  {  // programmatic dependent launch: setup, K/Q loads and the first MMAs
+     // overlap the row pass's tail
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = kTcSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if ((e = cudaLaunchKernelEx(&cfg, k1tc_colsum, p, tmQ, tmK))) return e;
+  }
   return cudaGetLastError();
 }
 
