@@ -149,3 +149,27 @@ def all_reduce_partial(x, world: int, group=None):
 
         dist.all_reduce(x, group=group)
     return x
+
+
+def lpt_assignment(costs, world: int) -> list:
+    """Longest-processing-time assignment of heads to ranks:
+    after profiling, a head's decode cost is its live-row count (kept + D);
+    heads go largest first to the least-loaded rank.  Returns, per rank, the
+    sorted head indices it owns; ties between ranks go to the lower rank, so
+    every rank computes the same assignment from the same costs."""
+    import heapq
+
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    order = sorted(range(len(costs)), key=lambda i: (-costs[i], i))
+    heap = [(0, r) for r in range(world)]
+    owned = [[] for _ in range(world)]
+    for i in order:
+        load, r = heapq.heappop(heap)
+        owned[r].append(i)
+        heapq.heappush(heap, (load + costs[i], r))
+    return [sorted(o) for o in owned]
+
+
+def assignment_loads(costs, owned) -> list:
+    return [sum(costs[i] for i in o) for o in owned]

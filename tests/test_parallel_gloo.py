@@ -84,3 +84,20 @@ def test_sharded_profile_equals_unsharded(tmp_path, mode):
     expect = profile_csv(sorted((b, h, p, float(r), int(c))
                                 for (b, h), (p, r, c) in zip(heads, full)))
     assert out.read_text() == expect
+
+
+def test_lpt_assignment_balances_ragged_heads():
+    from paper_2310_01801_b200.parallel import assignment_loads, lpt_assignment
+
+    rng = np.random.default_rng(0)
+    # config-1-like: most heads full (N + D), a few compressed ones
+    costs = [1536] * 240 + list(rng.integers(100, 900, size=16))
+    for world in (1, 2, 4, 8):
+        owned = lpt_assignment(costs, world)
+        assert sorted(i for o in owned for i in o) == list(range(len(costs)))
+        loads = assignment_loads(costs, owned)
+        assert max(loads) - min(loads) <= max(costs)
+        contiguous = [sum(costs[r * len(costs) // world:(r + 1) * len(costs) // world])
+                      for r in range(world)]
+        assert max(loads) <= max(contiguous)
+    assert lpt_assignment([5, 3, 3, 2, 2, 1], 2) == [[0, 3, 5], [1, 2, 4]]
