@@ -101,7 +101,7 @@ def main():
         model.decode_step()
     model.caches = []
 
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -111,12 +111,16 @@ def main():
     out = torch.empty(tokens.shape[0], D, dtype=torch.int64, device="cuda")
     for t in range(D):
         out[:, t] = model.decode_step()
+        if t == 0:
+            ev[3].record()   # the first step runs eagerly and captures the graphs
     mean_rec = model.mean_recovery() if args.diagnostics else None
     ev[2].record()
     torch.cuda.synchronize()
     model.check()
     prefill_ms = ev[0].elapsed_time(ev[1])
     decode_ms = ev[1].elapsed_time(ev[2])
+    first_ms = ev[1].elapsed_time(ev[3])
+    replay_ms = ev[3].elapsed_time(ev[2]) / max(D - 1, 1)
     prof_ms = pre.profiling_ms()
     b_local = tokens.shape[0]
     # full-policy heads hold exactly prompt + D rows; others no more
@@ -145,7 +149,8 @@ def main():
         local_heads=model.Hl, local_ffn=model.Fl,
         prefill_ms=prefill_ms, profiling_ms_per_layer=float(np.mean(prof_ms)),
         profiling_ms_total=float(np.sum(prof_ms)),
-        decode_ms=decode_ms, decode_ms_per_step=decode_ms / D, decode_tok_s=dec_tok_s,
+        decode_ms=decode_ms, decode_ms_per_step=decode_ms / D,
+        first_step_ms=first_ms, replay_ms_per_step=replay_ms, decode_tok_s=dec_tok_s,
         cache_tokens=cache_tokens, full_cache_tokens=full_tokens,
         pruned_ratio=1 - cache_tokens / full_tokens, policies=pol,
         deterministic=deterministic, full_heads_exact=bool(full_ok), live_bounded=bool(bound_ok),
