@@ -492,14 +492,16 @@ def bench_e2e(w, T, args, qh, kh, vh, clsh, slopes, sinks, dev, dist):
                 x[2 * rb:3 * rb].view(dt).view(B, H, d), x[3 * rb:3 * rb + B])
 
     # tensor views built once: the per-step host work is only the launch
-    dout = torch.empty(D, B, H, d, dtype=torch.float32, device=dev)
+    # two output buffers: a session's last output chunk drains to the host
+    # while the next session already runs
+    dout = [torch.empty(D, B, H, d, dtype=torch.float32, device=dev) for _ in range(2)]
     step_views = [[_views(rows[s][t]) for t in range(D)] for s in range(2)]
-    out_views = [dout[t] for t in range(D)]
+    out_views = [[dout[s][t] for t in range(D)] for s in range(2)]
     ev = lambda: torch.cuda.Event()
     ready, free = [ev(), ev()], [ev(), ev()]
     CH = 128
     chunk_done = [ev() for _ in range((D + CH - 1) // CH)]
-    out_free = ev()
+    out_free = [ev(), ev()]
     state = {"slot": 0}
 
     def upload(slot):
@@ -515,7 +517,7 @@ def bench_e2e(w, T, args, qh, kh, vh, clsh, slopes, sinks, dev, dist):
     def session(prefetch_next):
         slot = state["slot"]
         main.wait_event(ready[slot])
-        main.wait_event(out_free)  # the previous session's outputs have left dout
+        main.wait_event(out_free[slot])  # outputs of the session before last have left dout
         pool.reset()
         _, cache = encode_prompt_tensors(pq[slot], pk[slot], pv[slot], pc[slot], cfg,
                                          max_new_tokens=D, slopes=slopes, sinks=sinks, pool=pool)
@@ -524,21 +526,22 @@ def bench_e2e(w, T, args, qh, kh, vh, clsh, slopes, sinks, dev, dist):
         sv = step_views[slot]
         for t in range(D):
             q, k, v, c = sv[t]
-            decode_step_tensors(cache, q, k, v, c, out=out_views[t], chained=True)
+            decode_step_tensors(cache, q, k, v, c, out=out_views[slot][t], chained=True)
             if (t + 1) % CH == 0 or t + 1 == D:
                 c0 = (t // CH) * CH
                 e = chunk_done[t // CH]
                 e.record(main)
                 with torch.cuda.stream(cs):
                     cs.wait_event(e)
-                    hout[c0:t + 1].copy_(dout[c0:t + 1], non_blocking=True)
+                    hout[c0:t + 1].copy_(dout[slot][c0:t + 1], non_blocking=True)
         free[slot].record(main)
         with torch.cuda.stream(cs):
-            out_free.record(cs)
+            out_free[slot].record(cs)
         state["slot"] = slot ^ 1
         return cache
 
-    out_free.record(main)
+    for e_ in out_free:
+        e_.record(main)
     upload(0)
     for i in range(max(1, args.warmup)):
         session(prefetch_next=True)
