@@ -46,7 +46,7 @@ def launches(path, tag):
         name = r[i_n].split("(")[0].replace("void ", "")
         ks[name].append(float(r[i_v].replace(",", "")) / 1e3)
     tot = sum(sum(v) for v in ks.values())
-    out = [f"# {tag}: ncu launch list of `python bench.py --steps 2 --warmup 3 --no-cpu-baseline`",
+    out = [f"# {tag}: ncu launch list of `python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras` (tools/refresh_profiles.sh)",
            "", "`ncu --metrics gpu__time_duration.sum --clock-control none` (cold-cache, serialised:",
            "absolute times are pessimistic; the kernel SHARE of the step is what must agree).", "",
            f"{sum(len(v) for v in ks.values())} launches, {tot / 1e3:.1f} ms total", "",
