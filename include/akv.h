@@ -335,6 +335,17 @@ int akv_embed_classify(int32_t n, const int64_t* ids_dev, int32_t vocab, const u
 int akv_add_rmsnorm(int32_t rows, int32_t dim, int32_t dtype, const void* x_dev,
                     void* residual_dev, const void* w_dev, float eps, void* out_dev,
                     void* stream);
+/* Tensor-parallel decode: the all-reduce of row-parallel partial products
+ * fused with its consumer.  peer_ptrs_dev[r] (device array of n_peers
+ * addresses, rank order) points at rank r's [rows, peer_ld] partial -
+ * symmetric memory mapped over NVLink; the caller runs a cross-rank barrier
+ * after the partials are written.  residual += sum_r partial_r (fp32 sum in
+ * rank order, rounded to dtype: identical bits on every rank); out =
+ * residual * rsqrt(mean(residual^2) + eps) * w.  Replaces an all_reduce
+ * followed by akv_add_rmsnorm. */
+int akv_add_rmsnorm_peers(int32_t rows, int32_t dim, int32_t dtype, const uint64_t* peer_ptrs_dev,
+                          int32_t n_peers, int64_t peer_ld, void* residual_dev, const void* w_dev,
+                          float eps, void* out_dev, void* stream);
 typedef struct akv_rope_args {
   int32_t T;                  /* token rows of qkv; T % n == 0 */
   int32_t n;                  /* rows per sequence: token t = b*n + i */

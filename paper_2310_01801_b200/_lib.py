@@ -107,8 +107,8 @@ EXPORTS = (
     "akv_decode_recovery_workspace_init",
     "akv_softmax_rows_f64", "akv_causal_attention_f64", "akv_keep_mask", "akv_map_recovery_f64",
     "akv_update_scores_f64", "akv_gather_rows_f64", "akv_tv_distance_f64",
-    "akv_embed_classify", "akv_add_rmsnorm", "akv_rope_scatter", "akv_swiglu",
-    "akv_greedy_next", "akv_last_error", "akv_version", "akv_device_check",
+    "akv_embed_classify", "akv_add_rmsnorm", "akv_add_rmsnorm_peers", "akv_rope_scatter",
+    "akv_swiglu", "akv_greedy_next", "akv_last_error", "akv_version", "akv_device_check",
 )
 
 
@@ -149,6 +149,8 @@ def _load():
     lib.akv_decode_recovery_workspace_init.restype = C.c_int
     lib.akv_embed_classify.argtypes = [i32, P, i32, P, P, i32, i32, P, P, P]
     lib.akv_add_rmsnorm.argtypes = [i32, i32, i32, P, P, P, C.c_float, P, P]
+    lib.akv_add_rmsnorm_peers.argtypes = [i32, i32, i32, P, i32, i64, P, P, C.c_float, P, P]
+    lib.akv_add_rmsnorm_peers.restype = C.c_int
     lib.akv_rope_scatter.argtypes = [C.POINTER(RopeArgs), P]
     lib.akv_swiglu.argtypes = [i32, i32, i32, P, P, P]
     lib.akv_greedy_next.argtypes = [i32, i32, i32, P, i64, P, P, i32, P, P, P, P]

@@ -120,6 +120,67 @@ __global__ void __launch_bounds__(kRowThreads) k_add_rmsnorm(int dim, const T* x
   }
 }
 
+// Tensor-parallel reduction fused with the residual add and the RMSNorm
+// that consumes it: row `row` of every rank's row-parallel partial product
+// is read straight from that rank's (symmetric, peer-mapped) buffer - NVLink
+// loads - and summed in rank order in fp32, so every rank computes the same
+// bits; then residual += sum (rounded to T like the NCCL all-reduce result)
+// and out = rmsnorm(residual) * w.  Replaces all_reduce + akv_add_rmsnorm.
+template <typename T>
+__global__ void __launch_bounds__(kRowThreads) k_peer_add_rmsnorm(int dim, const uint64_t* peers,
+                                                                  int n_peers, int64_t peer_ld,
+                                                                  T* res, const T* w, float eps,
+                                                                  T* out) {
+  __shared__ float red[kRowThreads / 32];
+  constexpr int n = Vec16<T>::n;
+  const int64_t base = (int64_t)blockIdx.x * dim;
+  const int nv = dim / n;
+  float v[kMaxVecPerThread][n];
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < kMaxVecPerThread; ++j) {
+    const int iv = threadIdx.x + j * kRowThreads;
+    if (iv < nv) {
+      float a[n];
+#pragma unroll
+      for (int e = 0; e < n; ++e) a[e] = 0.f;
+      for (int r = 0; r < n_peers; ++r) {
+        const T* src = reinterpret_cast<const T*>(peers[r]) + (int64_t)blockIdx.x * peer_ld;
+        // another GPU wrote it: fetch past any cached copy (ld.global.cv)
+        const uint4 u = __ldcv(reinterpret_cast<const uint4*>(src + iv * n));
+        float f[n];
+        if constexpr (n == 4) {
+          f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y);
+          f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);
+        } else {
+          Elem<__nv_bfloat16>::unpack(u, f);
+        }
+#pragma unroll
+        for (int e = 0; e < n; ++e) a[e] += f[e];
+      }
+      Vec16<T>::load(res + base + iv * n, v[j]);
+#pragma unroll
+      for (int e = 0; e < n; ++e) v[j][e] = to_f(from_f<T>(v[j][e] + to_f(from_f<T>(a[e]))));
+      Vec16<T>::store(res + base + iv * n, v[j]);
+#pragma unroll
+      for (int e = 0; e < n; ++e) ss = fmaf(v[j][e], v[j][e], ss);
+    }
+  }
+  ss = block_sum(ss, red);
+  const float rs = rsqrtf(ss / (float)dim + eps);
+#pragma unroll
+  for (int j = 0; j < kMaxVecPerThread; ++j) {
+    const int iv = threadIdx.x + j * kRowThreads;
+    if (iv < nv) {
+      float g[n];
+      Vec16<T>::load(w + iv * n, g);
+#pragma unroll
+      for (int e = 0; e < n; ++e) g[e] *= v[j][e] * rs;
+      Vec16<T>::store(out + base + iv * n, g);
+    }
+  }
+}
+
 // RoPE (rotate-half pairing c <-> c + d/2) of q and k, copy of v; token t =
 // b*n + i sits at position pos0 + i and lands in row row0 + i of head h of
 // batch row b.  128 threads = (128 / (d/2)) heads x d/2 pairs.
@@ -279,6 +340,33 @@ extern "C" int akv_add_rmsnorm(int32_t rows, int32_t dim, int32_t dtype, const v
   else
     return set_error(AKV_ERR_UNSUPPORTED, "akv_add_rmsnorm: dtype %d", dtype);
   return launch_status("akv_add_rmsnorm");
+}
+
+extern "C" int akv_add_rmsnorm_peers(int32_t rows, int32_t dim, int32_t dtype,
+                                     const uint64_t* peer_ptrs_dev, int32_t n_peers,
+                                     int64_t peer_ld, void* residual_dev, const void* w_dev,
+                                     float eps, void* out_dev, void* stream) {
+  if (rows < 0 || dim < 1 || n_peers < 1 || peer_ld < dim || !peer_ptrs_dev || !residual_dev ||
+      !w_dev || !out_dev)
+    return set_error(AKV_ERR_INVALID, "akv_add_rmsnorm_peers: bad arguments");
+  if (rows == 0) return AKV_OK;
+  const int vec = dtype == AKV_DTYPE_F32 ? 4 : 8;
+  if (dim % vec || peer_ld % vec || dim > vec * kRowThreads * kMaxVecPerThread ||
+      !aligned16(residual_dev) || !aligned16(out_dev) || !aligned16(w_dev))
+    return set_error(AKV_ERR_UNSUPPORTED, "akv_add_rmsnorm_peers: dim %d unsupported for dtype %d",
+                     dim, dtype);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == AKV_DTYPE_F32)
+    k_peer_add_rmsnorm<float><<<rows, kRowThreads, 0, st>>>(
+        dim, peer_ptrs_dev, n_peers, peer_ld, (float*)residual_dev, (const float*)w_dev, eps,
+        (float*)out_dev);
+  else if (dtype == AKV_DTYPE_BF16)
+    k_peer_add_rmsnorm<__nv_bfloat16><<<rows, kRowThreads, 0, st>>>(
+        dim, peer_ptrs_dev, n_peers, peer_ld, (__nv_bfloat16*)residual_dev,
+        (const __nv_bfloat16*)w_dev, eps, (__nv_bfloat16*)out_dev);
+  else
+    return set_error(AKV_ERR_UNSUPPORTED, "akv_add_rmsnorm_peers: dtype %d", dtype);
+  return launch_status("akv_add_rmsnorm_peers");
 }
 
 extern "C" int akv_rope_scatter(const akv_rope_args* a, void* stream) {

@@ -127,6 +127,13 @@ class _Layer:
 
 
 @dataclass
+class _PeerPartials:
+    """Pending tensor-parallel reduction: slot of the symmetric buffers that
+    hold every rank's partial product (consumed by _rmsnorm)."""
+    slot: int
+
+
+@dataclass
 class PrefillResult:
     profiles: list                     # per layer: ProfileResult (local heads)
     next_tokens: torch.Tensor          # [B] int64 (device)
@@ -171,6 +178,7 @@ class FastGenLlama:
         self.record = False
         self.use_graphs = True
         self._graphs = None
+        self._ar_bufs = None      # tensor-parallel decode reduction buffers (_setup_tp_reduce)
         self.pos_dev = None
         self.trace: dict = {}
 
@@ -213,6 +221,13 @@ class FastGenLlama:
     def _rmsnorm(self, residual, w, x=None, out=None):
         rows, dim = residual.shape
         out = torch.empty_like(residual) if out is None else out
+        if isinstance(x, _PeerPartials):   # tensor-parallel reduction fused into the norm
+            ptrs = self._ar_ptrs[x.slot]
+            check(lib.akv_add_rmsnorm_peers(rows, dim, self.dt, _ptr(ptrs), ptrs.numel(),
+                                            self._ar_bufs[x.slot].stride(0), _ptr(residual),
+                                            _ptr(w), self.cfg.eps, _ptr(out), _stream()),
+                  EngineError)
+            return out
         check(lib.akv_add_rmsnorm(rows, dim, self.dt, _ptr(x), _ptr(residual), _ptr(w),
                                   self.cfg.eps, _ptr(out), _stream()), EngineError)
         return out
@@ -302,11 +317,56 @@ class FastGenLlama:
             return x
         return all_reduce_partial(x, self.plan.world, self.group)
 
+    def _setup_tp_reduce(self, B, local=False):
+        """Decode-time row-parallel reductions (tp mode) fused into the norm
+        that consumes them: each rank's O / down projection writes its
+        partial product into its own symmetric-memory buffer [B, dm] (two
+        alternating, so one barrier per reduction also orders the reuse),
+        a device-side barrier, then akv_add_rmsnorm_peers sums every rank's
+        partial over NVLink loads (rank order: identical bits everywhere),
+        adds the residual and normalises - no NCCL call on the decode path.
+        ``local`` builds the same plumbing over this process's buffers only
+        (world 1; tests)."""
+        self._ar_bufs = None
+        multi = self.plan.mode == "tp" and self.plan.comm and self.plan.world > 1
+        if not (multi or local):
+            return
+        dm = self.cfg.d_model
+        bufs, ptrs, hdls = [], [], []
+        for i in range(2):
+            if multi:
+                import torch.distributed as dist
+                import torch.distributed._symmetric_memory as symm_mem
+
+                group = self.group if self.group is not None else dist.group.WORLD
+                t = symm_mem.empty((B, dm), dtype=self.dtype, device=self.device)
+                hdl = symm_mem.rendezvous(t, group.group_name)
+                p = list(hdl.buffer_ptrs)
+            else:
+                t = torch.zeros(B, dm, dtype=self.dtype, device=self.device)
+                hdl, p = None, [t.data_ptr()]
+            bufs.append(t)
+            hdls.append(hdl)
+            ptrs.append(torch.tensor(p, dtype=torch.int64, device=self.device))
+        self._ar_bufs, self._ar_ptrs, self._ar_hdls, self._ar_next = bufs, ptrs, hdls, 0
+
+    def _reduce_linear(self, x, w):
+        """x @ w.T summed over the tensor-parallel ranks: a _PeerPartials
+        handle for the fused decode path, else the all-reduced tensor."""
+        if self._ar_bufs is not None and x.shape[0] == self._ar_bufs[0].shape[0]:
+            slot = self._ar_next
+            self._ar_next ^= 1
+            torch.matmul(x, w.t(), out=self._ar_bufs[slot])
+            if self._ar_hdls[slot] is not None:
+                self._ar_hdls[slot].barrier(channel=slot)
+            return _PeerPartials(slot)
+        return self._reduce(torch.nn.functional.linear(x, w))
+
     def _mlp(self, L, residual, attn_out):
         """residual += attn_out; MLP; returns (mlp delta)."""
         xn = self._rmsnorm(residual, L.mlp_norm, x=attn_out)
         gu = torch.nn.functional.linear(xn, L.wgu)
-        return self._reduce(torch.nn.functional.linear(self._swiglu(gu), L.wdown))
+        return self._reduce_linear(self._swiglu(gu), L.wdown)
 
     # -- prefill ------------------------------------------------------------
     def prefill(self, tokens: torch.Tensor, profiler_cfg: ProfilerConfig | None = None,
@@ -347,6 +407,7 @@ class FastGenLlama:
         k, v = torch.empty_like(q), torch.empty_like(q)
         self.caches, profiles, prof_events = [], [], []
         self._graphs = None
+        self._ar_bufs = None      # prefill reduces through NCCL
         self.trace = {"prompt": [], "steps": []} if self.record else {}
         delta = None
         for li, L in enumerate(self.layers):
@@ -385,6 +446,7 @@ class FastGenLlama:
         self.o_dec = torch.empty(len(self.layers), B, self.Hl, d, dtype=torch.float32,
                                  device=self.device)
         self._setup_decode_gather(B)
+        self._setup_tp_reduce(B)
         out = PrefillResult(profiles, self.next_tok)
         out.events = prof_events
         return out
@@ -436,7 +498,7 @@ class FastGenLlama:
                     rec.append((self.q1.clone(), self.k1.clone(), self.v1.clone()))
                 o = decode_step_tensors(self.caches[li], self.q1, self.k1, self.v1, new_cls,
                                         out=self.o_dec[li])
-            attn = self._reduce(torch.nn.functional.linear(self._decode_gathered(li), L.wo))
+            attn = self._reduce_linear(self._decode_gathered(li), L.wo)
             delta = self._mlp(L, residual, attn)
         xf = self._rmsnorm(residual, self.final_norm, x=delta)
         logits = torch.nn.functional.linear(xf, self.lm_head)

@@ -258,3 +258,72 @@ def test_decode_writes_outputs_to_peer_buffers(dtype):
             ref = o.to(dtype).float()
             assert torch.equal(got, ref)
             assert (buf[:, :col0] == -7).all() and (buf[:, col0 + H * d:] == -7).all()
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_peer_reduction_fused_into_rmsnorm(dtype):
+    """akv_add_rmsnorm_peers: residual += sum of the ranks' partials (fp32 in
+    rank order, rounded once), then RMSNorm - here 1-3 local buffers stand in
+    for the ranks' symmetric-memory buffers.  With one partial it is bitwise
+    akv_add_rmsnorm."""
+    import ctypes as C
+
+    from paper_2310_01801_b200._lib import check, lib
+
+    g = torch.Generator(device="cuda").manual_seed(11)
+    rows, dm, ld, eps = 7, 1024, 1040, 1e-5
+    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    w = (1 + 0.1 * torch.randn(dm, device="cuda", generator=g)).to(dtype)
+    res0 = torch.randn(rows, dm, device="cuda", generator=g).to(dtype)
+    dt = 0 if dtype == torch.float32 else 1
+    tol = 1e-5 if dtype == torch.float32 else 2e-2
+    for P in (1, 2, 3):
+        parts = [torch.randn(rows, ld, device="cuda", generator=g).to(dtype) for _ in range(P)]
+        ptrs = torch.tensor([t.data_ptr() for t in parts], dtype=torch.int64, device="cuda")
+        res, out = res0.clone(), torch.empty_like(res0)
+        check(lib.akv_add_rmsnorm_peers(rows, dm, dt, C.c_void_p(ptrs.data_ptr()), P, ld,
+                                        C.c_void_p(res.data_ptr()), C.c_void_p(w.data_ptr()), eps,
+                                        C.c_void_p(out.data_ptr()), stream))
+        s = torch.zeros(rows, dm, device="cuda")
+        for t in parts:
+            s += t[:, :dm].float()
+        h = (res0.float() + s.to(dtype).float()).to(dtype).float()
+        ref = h * torch.rsqrt(h.pow(2).mean(-1, keepdim=True) + eps) * w.float()
+        assert torch.equal(res.float(), h)
+        assert torch.allclose(out.float(), ref, rtol=tol, atol=tol)
+        if P == 1:
+            res2, out2 = res0.clone(), torch.empty_like(res0)
+            x = parts[0][:, :dm].contiguous()
+            check(lib.akv_add_rmsnorm(rows, dm, dt, C.c_void_p(x.data_ptr()),
+                                      C.c_void_p(res2.data_ptr()), C.c_void_p(w.data_ptr()), eps,
+                                      C.c_void_p(out2.data_ptr()), stream))
+            assert torch.equal(res2, res) and torch.equal(out2, out)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_tp_decode_with_fused_peer_reduction(dtype):
+    """Tensor-parallel decode plumbing of FastGenLlama (row-parallel partial
+    products in alternating reduction buffers, consumed by
+    akv_add_rmsnorm_peers) on one rank: bit-identical logits and tokens to
+    the unfused path, eager step and graph replays alike."""
+    from paper_2310_01801_b200 import ProfilerConfig
+    from paper_2310_01801_b200.llama import FastGenLlama, ShardPlan
+
+    cfg = _tiny()
+    tokens = _prompt(3, 24, cfg.vocab, seed=5)
+    runs = []
+    for fused in (False, True):
+        m = FastGenLlama(cfg, dtype=dtype, seed=7, special_ids=SPECIAL, punct_ids=PUNCT,
+                         max_positions=64, plan=ShardPlan(0, 1, "tp", True))
+        m.prefill(tokens, ProfilerConfig(recovery_threshold=0.95), max_new_tokens=5)
+        if fused:
+            m._setup_tp_reduce(m.B, local=True)
+            assert m._ar_bufs is not None
+        toks, logits = [], []
+        for _ in range(5):
+            toks.append(m.decode_step())
+            logits.append(m.last_logits.clone())
+        m.check()
+        runs.append((torch.stack(toks), torch.stack(logits)))
+    assert torch.equal(runs[0][0], runs[1][0])
+    assert torch.equal(runs[0][1], runs[1][1])
