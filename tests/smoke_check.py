@@ -22,7 +22,7 @@ def run_smoke():
     w, opts = C.case_workload(name)
     g = dict(R=o["R"], cost=o["cost"], colsum=o["colsum"], dec_choice=o["dec_choice"],
              choice=o["choice"], enc_kept=o["enc_kept"], enc_out=o["enc_out"],
-             dec_kept=o["dec_kept"], dec_out=o["dec_out"])
+             dec_kept=o["dec_kept"], dec_out=o["dec_out"], dec_rec=o["dec_rec"])
     excluded = _compare(name, g, r, w, opts)
     print(f"smoke ok: {name} on {torch.cuda.get_device_name(0)} in {time.time() - t0:.2f}s; "
           f"policies {np.bincount(r['res'].choice[:, 0], minlength=5).tolist()}, "

@@ -74,3 +74,22 @@ def test_compute_entry_points_fail_loudly_without_device():
     rc = _lib.lib.akv_device_check()
     assert rc != _lib.AKV_OK
     assert _lib.lib.akv_last_error()
+
+
+def test_smoke_reference_covers_every_compared_field():
+    """smoke() builds its reference from the oracle; it must carry every
+    field test_gpu_parity._compare reads (a missing key only shows on the
+    GPU box at round end)."""
+    import ast
+    import inspect
+
+    import smoke_check
+    import test_gpu_parity
+
+    src = inspect.getsource(test_gpu_parity._compare)
+    used = {n.slice.value for n in ast.walk(ast.parse(src))
+            if isinstance(n, ast.Subscript) and isinstance(n.value, ast.Name) and n.value.id == "g"
+            and isinstance(n.slice, ast.Constant)}
+    smoke_src = inspect.getsource(smoke_check.run_smoke)
+    missing = [k for k in used if f"{k}=" not in smoke_src]
+    assert not missing, missing
