@@ -200,11 +200,20 @@ def bench_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
+    # AKV_BENCH_ONE_DEVICE=1 (code-path check only): every rank on cuda:0 over
+    # gloo, so the torchrun path can be exercised on a one-GPU box; its
+    # numbers are not measurements
+    one_dev = os.environ.get("AKV_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     if world > 1:
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     w = config1(seed=1 + rank)
@@ -588,13 +597,19 @@ def _oracle_heads(args):
     cls = class_lut()[w.tokens(b)].astype(np.int64)
     data = [tuple(x.astype(np.float64) for x in w.head_qkv(b, h)) for h in heads]
     fam = O.default_family(w.r_l, w.r_f)
-    t0 = time.perf_counter()
-    for h, (q, k, v) in zip(heads, data):
-        prof = O.profile_head(q[:N], k[:N], v[:N], cls, w.slopes[h], w.sinks[h], fam, [T])
-        st = O.compact_head(prof, k[:N], v[:N], fam[prof.choice[0]], N, w.slopes[h], w.sinks[h])
-        for t in range(D):
-            O.decode_head(st, q[N + t], k[N + t], v[N + t], N + t, cls, N)
-    return time.perf_counter() - t0
+    from threadpoolctl import threadpool_limits
+
+    # one BLAS thread per process: `cores` counts processes, and a pool of
+    # multi-threaded workers would oversubscribe the host
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        for h, (q, k, v) in zip(heads, data):
+            prof = O.profile_head(q[:N], k[:N], v[:N], cls, w.slopes[h], w.sinks[h], fam, [T])
+            st = O.compact_head(prof, k[:N], v[:N], fam[prof.choice[0]], N, w.slopes[h],
+                                w.sinks[h])
+            for t in range(D):
+                O.decode_head(st, q[N + t], k[N + t], v[N + t], N + t, cls, N)
+        return time.perf_counter() - t0
 
 
 def cpu_baseline_port(w, T):
