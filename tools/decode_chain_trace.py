@@ -46,7 +46,9 @@ def main():
         rel = (tr[ok, :5] - t0) / 1e3
         q = lambda col, p: np.percentile(rel[:, col], p)  # noqa: E731
         print(f"step {at + k}: CTAs {ok.sum()}  start [{q(0, 0):6.1f} {q(0, 50):6.1f} {q(0, 100):6.1f}]"
-              f"  first page [{q(2, 0):6.1f} {q(2, 50):6.1f}]  last page [{q(3, 50):6.1f} {q(3, 100):6.1f}]"
+              f"  planned-start {np.median(rel[:, 1] - rel[:, 0]):5.2f}"
+              f"  first page [{q(2, 0):6.1f} {q(2, 50):6.1f}] (-start {np.median(rel[:, 2] - rel[:, 0]):5.2f})"
+              f"  last page [{q(3, 50):6.1f} {q(3, 100):6.1f}]"
               f"  done [{q(4, 50):6.1f} {q(4, 90):6.1f} {q(4, 100):6.1f}]")
 
 
