@@ -352,6 +352,10 @@ def bench_ours(args):
             "avg_launch_ms": k1_avg,
             "note": "2*B*H*d*N(N+1): both causal QK^T passes; the exp/softmax epilogue, not the "
                     "MMA, sets the pace at N=1024 (config 4, N=16384: ~0.67 PFLOP/s)",
+            # the bound that binds: B*H*N(N+1) exponentials (both passes) against the
+            # nominal MUFU rate of 16 ex2/clk/SM at the sampled SM clock;
+            # a quarter of the row pass's exponentials run on the FMA pipe instead
+            "exp": _exp_roofline(w, k1_avg, clk),
         },
         "clocks": clk.summary(),
         "wall_s": t_wall,
@@ -456,6 +460,19 @@ def bench_extras(T, dev, peaks):
     del model
     torch.cuda.empty_cache()
     return out
+
+
+def _exp_roofline(w, k1_ms, clk):
+    import torch
+
+    exps = float(w.B * w.H * w.N * (w.N + 1))
+    mhz = (clk.summary() or {}).get("sm_mhz") or 1965.0
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    peak = 16.0 * sms * mhz * 1e6 / 1e9   # Gexp/s
+    ach = exps / (k1_ms * 1e-3) / 1e9
+    return {"achieved": ach, "peak": peak, "unit": "Gexp/s", "frac": ach / peak,
+            "peak_kind": "nominal: 16 ex2/clk/SM x SMs x sampled SM clock",
+            "exps_per_launch": exps}
 
 
 def bench_e2e(w, T, args, qh, kh, vh, clsh, slopes, sinks, dev, dist):
