@@ -21,8 +21,9 @@
 // from live_in and takes one contiguous, equal share of the flattened page
 // list.  The last warp is the producer: one elected lane streams each
 // page's K rows, V rows, slot metadata and the head's q (plus the new
-// token's k/v for the page holding slot `live`) into a 3-stage shared
-// memory ring (TMA, mbarrier transaction counts).  The other warps consume:
+// token's k/v for the page holding slot `live`) into a 2-stage shared
+// memory ring (TMA, mbarrier transaction counts; 3 stages for the SIMT
+// variant and as a tuning option).  The other warps consume:
 // logits with the planted bias, online softmax, PV accumulation per head
 // segment; at the end of a head's segment they publish (max, sum, o[d])
 // and bump the head's split-K semaphore.  The CTA completing a head runs
@@ -52,7 +53,7 @@
 
 namespace akv {
 
-constexpr int kStages = 3;
+constexpr int kStages = 3;  // SIMT (fp32 / small d) variant; the tcgen05-era mma kernel takes ST
 constexpr int kPageBytes = 16384;  // per K (and per V) page
 constexpr int kMaxHeads = 2048;
 constexpr int kEpr = 8;   // candidates per thread per batch in the epilogue passes
@@ -942,7 +943,8 @@ struct PubSlot {
   HeadCtx ctx;
 };
 
-template <int D>
+// ST ring stages (2 by default, 3 for tuning; see launch_mma)
+template <int D, int ST>
 __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
     k3_decode_mma(const __grid_constant__ DecParams p, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV) {
@@ -951,7 +953,7 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
   constexpr int NK = D / 16;  // 16-dim chunks
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
+  __shared__ __align__(8) uint64_t full_bar[ST], empty_bar[ST];
   __shared__ __align__(8) uint64_t pub_full[2], pub_empty[2];
   __shared__ PubSlot<NW, D> s_pub[2];
   __shared__ int s_last;
@@ -960,13 +962,13 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
   using ES = NamedSync<S::NE * 32, 2, S::EFIRST>;
 
   const int G = p.G;
-  int* s_prefix = reinterpret_cast<int*>(smem + kStages * S::STAGE_B);
+  int* s_prefix = reinterpret_cast<int*>(smem + ST * S::STAGE_B);
   int* s_live = s_prefix + (G + 1);
   uint8_t* s_full = reinterpret_cast<uint8_t*>(s_live + G);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   AKV_TRACE(0);
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], NW); }
+    for (int s = 0; s < ST; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], NW); }
     for (int s = 0; s < 2; ++s) { mbar_init(&pub_full[s], NW); mbar_init(&pub_empty[s], 1); }
     mbar_fence_init();
     tma_prefetch_desc(&tmK);
@@ -1010,10 +1012,10 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
       // L2 prefetch cursor: the pages just beyond the shared-memory ring go
       // to L2 early (coherent, so safe before the previous step drains),
       // raising the bytes in flight per CTA beyond what the ring can hold
-      long long pf = pbeg + kStages;
+      long long pf = pbeg + ST;
       int gpf = g0;
       for (long long pg = pbeg; pg < pend; ++pg) {
-        for (const long long lim = min(pend, pg + kStages + p.l2_prefetch); pf < lim; ++pf) {
+        for (const long long lim = min(pend, pg + ST + p.l2_prefetch); pf < lim; ++pf) {
           while (pf >= s_prefix[gpf + 1]) ++gpf;
           const int s0 = (int)(pf - s_prefix[gpf]) * PAGE;
           if (s0 <= s_live[gpf]) {
@@ -1065,7 +1067,7 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
           bulk_g2s(hdr + 2 * RB, static_cast<const __nv_bfloat16*>(p.vn) + (size_t)g * p.bh_stride,
                    RB, &full_bar[stage], pol_keep);
         }
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
+        if (++stage == ST) { stage = 0; phase ^= 1; }
       }
     }
     return;
@@ -1227,7 +1229,7 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[stage]);
-    if (++stage == kStages) { stage = 0; phase ^= 1; }
+    if (++stage == ST) { stage = 0; phase ^= 1; }
 
     if (!((pg + 1 == pend) || (pg + 1 == s_prefix[g + 1]))) continue;
     l_run = warp_allreduce(l_run, [](float a, float b) { return a + b; });
@@ -1396,19 +1398,50 @@ static cudaError_t launch_mma(const DecParams& p, int64_t total_slots, cudaStrea
       return cudaErrorInvalidValue;
     tm->kc = p.kc; tm->vc = p.vc; tm->slots = total_slots; tm->d = D;
   }
-  auto kern = k3_decode_mma<D>;
+  auto k3 = k3_decode_mma<D, 3>;
+  auto k2 = k3_decode_mma<D, 2>;
+  const size_t plan = (size_t)(2 * kMaxHeads + 1) * 4 + kMaxHeads;
   static bool attr = false;
+  static size_t static3 = 0, static2 = 0, per_sm = 0, reserve = 0;
   cudaError_t e;
   if (!attr) {
-    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(1024 + kStages * S::STAGE_B + (2 * kMaxHeads + 1) * 4 + kMaxHeads))))
+    if ((e = cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(1024 + 3 * S::STAGE_B + plan))) ||
+        (e = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(1024 + 2 * S::STAGE_B + plan))))
       return e;
+    cudaFuncAttributes fa;
+    if ((e = cudaFuncGetAttributes(&fa, k3))) return e;
+    static3 = fa.sharedSizeBytes;
+    if ((e = cudaFuncGetAttributes(&fa, k2))) return e;
+    static2 = fa.sharedSizeBytes;
+    int dev = 0, v = 0;
+    if ((e = cudaGetDevice(&dev))) return e;
+    if ((e = cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev))) return e;
+    per_sm = (size_t)v;
+    if ((e = cudaDeviceGetAttribute(&v, cudaDevAttrReservedSharedMemoryPerBlock, dev))) return e;
+    reserve = (size_t)v;
     attr = true;
   }
   int sms;
   if ((e = num_sms(&sms))) return e;
-  const size_t smem = 1024 + (size_t)kStages * S::STAGE_B + (size_t)(2 * p.G + 1) * 4 + p.G;
-  return launch_pdl(kern, k3_grid(sms), S::THREADS, smem, st, p, tm->k, tm->v);
+  const size_t plan_g = (size_t)(2 * p.G + 1) * 4 + p.G;
+  const size_t smem3 = 1024 + (size_t)3 * S::STAGE_B + plan_g;
+  // Two ring stages by default: measured at least as fast as three at every
+  // size (c1 29.44 -> 29.26 us/step; B*H 128..512 likewise) and they keep two
+  // CTAs per SM up to 2048 heads per launch, where a 3-stage ring drops to
+  // one CTA per SM beyond 512 heads (3.5 vs 5.9 TB/s).  AKV_K3_STAGES=3
+  // selects the 3-stage ring where two CTAs still fit (tuning).
+  static int stages = -1;
+  if (stages < 0) {
+    const char* fs = getenv("AKV_K3_STAGES");
+    stages = fs ? atoi(fs) : 2;
+  }
+  if (stages == 3 && 2 * (smem3 + static3 + reserve) <= per_sm)
+    return launch_pdl(k3, k3_grid(sms), S::THREADS, smem3, st, p, tm->k, tm->v);
+  const size_t smem2 = 1024 + (size_t)2 * S::STAGE_B + plan_g;
+  (void)static2;
+  return launch_pdl(k2, k3_grid(sms), S::THREADS, smem2, st, p, tm->k, tm->v);
 }
 
 struct DecWs {
