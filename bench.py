@@ -329,14 +329,14 @@ def bench_ours(args):
         "sweep": sweep,
         "gpu_launches": args.steps * (5 + D),
         "roofline": {
-            "kernel": "k3_decode (akv_decode_step)",
+            "kernel": "k3_decode_mma<128, 2> (akv_decode_step)",
             "bound": "hbm",
             "achieved": achieved,
             "peak": peaks.get("hbm_gbs"),
             "peak_kind": peak_kind,
             "unit": "GB/s",
             "frac": achieved / peaks.get("hbm_gbs"),
-            "traffic": _traffic("k3_decode_mma<128>"),
+            "traffic": _traffic("k3_decode_mma<128, 2>"),
             "algorithmic_bytes_per_launch": avg_bytes,
             "avg_launch_us": launch_us,
         },
