@@ -14,7 +14,7 @@ from .engine import (ArenaPool, CompressedCache, EngineError, GenerationConfig, 
                      HeadCacheState,
                      GreedyArgmax, Nucleus, ProfileResult, StepRecord, decode_step_tensors,
                      encode_prompt, encode_prompt_tensors, generate, generate_fixed_baseline,
-                     generate_step, records_to_ndjson, reference_generate)
+                     generate_step, grow_cache, records_to_ndjson, reference_generate)
 from .policies import (DEFAULT_FEASIBLE_ORDER, DEFAULT_RATIO, CompressionPolicy, PolicyAtom,
                        PolicyContext, PolicyError, RetainedSet, apply_policy, cache_memory_cost,
                        feasible_set, format_policy, full_policy, local_budget, parse_policy,

@@ -534,6 +534,66 @@ def encode_prompt_tensors(q, k, v, classes, profiler_cfg: ProfilerConfig | None 
     return res, cache
 
 
+def grow_cache(cache: CompressedCache, extra_steps: int) -> None:
+    """Room for ``extra_steps`` more decode steps.  The reference's per-head
+    lists grow without bound (engine.py:315-317); here every head's segment
+    gains ``extra_steps`` slots (rounded up to 8), the segments move to a new
+    private arena (a device-side gather of each old segment), and the decode
+    workspace - plus, in diagnostics mode, the position-indexed shadow keys
+    and class history - are rebuilt.  The session continues bit-identically.
+    One device->host read (the new arena size); not for a cache whose decode
+    is captured in a CUDA graph (its pointers change)."""
+    if extra_steps <= 0:
+        return
+    cache.check()
+    dev, G, d = cache.device, cache.G, cache.d
+    i64 = torch.int64
+    old_cap = cache.seg_cap.to(i64)
+    old_off = cache.seg_off.to(i64)
+    new_cap = ((old_cap + int(extra_steps) + 7) // 8) * 8
+    new_off = torch.cumsum(new_cap, 0) - new_cap
+    total = max(int(new_cap.sum().item()), 1)
+    n_old = int(old_cap.sum().item())
+    seg = torch.repeat_interleave(torch.arange(G, device=dev), old_cap, output_size=n_old)
+    j = torch.arange(n_old, device=dev) - (torch.cumsum(old_cap, 0) - old_cap)[seg]
+    src, dst = old_off[seg] + j, new_off[seg] + j
+    for name, width in (("kc", d), ("vc", d), ("meta", None), ("score", None)):
+        old = getattr(cache, name)
+        new = torch.empty((total, width) if width else (total,), dtype=old.dtype, device=dev)
+        new[dst] = old[src]
+        setattr(cache, name, new)
+    cache.pool = None
+    cache.seg_cap = new_cap.to(torch.int32)
+    cache.seg_off = new_off
+    cache.total_slots = total
+    cache.max_cap = int(((cache.max_cap + int(extra_steps) + 7) // 8) * 8)
+    cache.capacity_steps += int(extra_steps)
+    B, H = cache.B, cache.H
+    ws_bytes = lib.akv_decode_workspace_size(B, H, d, cache.max_cap, cache.total_slots)
+    cache.workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    check(lib.akv_decode_workspace_init(_ptr(cache.workspace), ws_bytes, B, H, d, cache.max_cap,
+                                        cache.total_slots, _stream()), EngineError)
+    dt = DTYPE_BF16 if cache.dtype == torch.bfloat16 else DTYPE_F32
+    cache._dargs = _decode_args(cache, dt)
+    if cache.track_recovery:
+        old_ld = cache.shadow.shape[1]
+        ld = old_ld + int(extra_steps)
+        shadow = torch.empty(G, ld, d, dtype=cache.shadow.dtype, device=dev)
+        shadow[:, :old_ld].copy_(cache.shadow)
+        cls_hist = torch.zeros(B, ld, dtype=torch.uint8, device=dev)
+        cls_hist[:, :old_ld].copy_(cache.cls_hist)
+        cache.shadow, cache.cls_hist = shadow, cls_hist
+        ws = lib.akv_decode_recovery_workspace_size(B, H, ld)
+        cache.diag_ws = torch.empty(ws, dtype=torch.uint8, device=dev)
+        check(lib.akv_decode_recovery_workspace_init(_ptr(cache.diag_ws), ws, B, H, ld, _stream()),
+              EngineError)
+        g = cache._diag_args
+        g.seg_off_dev, g.meta_dev = _ptr(cache.seg_off), _ptr(cache.meta)
+        g.shadow_dev, g.shadow_ld = _ptr(cache.shadow), ld
+        g.cls_hist_dev, g.cls_ld = _ptr(cache.cls_hist), ld
+        g.workspace_dev, g.workspace_bytes = _ptr(cache.diag_ws), ws
+
+
 def _launch_recovery(cache, q, k, new_classes, live_in, pos=None, pos_dev=None):
     """Before the decode step of the same position (pre-eviction live set)."""
     g = cache._diag_args
@@ -751,6 +811,9 @@ def generate_step(model, cache: CompressedCache, last_token=None, sampler=None):
         kd = torch.from_numpy(k[:, :, 0]).to(dev)
         vd = torch.from_numpy(v[:, :, 0]).to(dev)
         cache._model_new_cls.fill_(CLASS_CODE[klass])
+        if cache.seq_len - cache.prompt_len >= cache.capacity_steps:
+            # the reference's cache is unbounded: double the decode room
+            grow_cache(cache, max(cache.capacity_steps, 16))
         decode_step_tensors(cache, qd.to(cache.dtype), kd.to(cache.dtype), vd.to(cache.dtype),
                             cache._model_new_cls)
     concat = cache.out.reshape(-1).double().cpu().numpy()
