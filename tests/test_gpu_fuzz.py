@@ -40,11 +40,15 @@ def _case(seed):
     B = int(rng.integers(1, 3))
     H = int(rng.integers(1, 5))
     d = int(rng.choice([16, 32, 64, 128]))
+    if seed >= WIDE_BASE:   # many heads per launch (several heads per CTA, large page plans)
+        B, H, d = int(rng.choice([8, 16, 24])), int(rng.choice([16, 32])), int(rng.choice([64, 128]))
     sizes = [1, 2, 7, 33, 64, 129, 200, 300]
-    if seed >= LARGE_BASE:   # the large sweep: multi-page segments, long budgets
+    if seed >= WIDE_BASE:
+        sizes = [16, 33, 64, 130]
+    elif seed >= LARGE_BASE:   # the large sweep: multi-page segments, long budgets
         sizes = [255, 511, 640, 1024, 1500]
     N = int(rng.choice(sizes))
-    D = int(rng.integers(0, 25))
+    D = int(rng.integers(0, 25)) if seed < WIDE_BASE else int(rng.integers(1, 9))
     dtype = "bf16" if rng.random() < 0.5 else "f32"
     order = list(rng.permutation(ATOMS))
     if rng.random() < 0.3:
@@ -66,9 +70,34 @@ def _case(seed):
                 q=x[0], k=x[1], v=x[2], slopes=slopes, sinks=sinks, cls=cls)
 
 
+# relative score gap at the frequent boundary below which a decode step's
+# kept set may legitimately differ: the GPU's per-step attention weights come
+# from fp32 logits (~5e-5 relative error in the accumulated scores at bf16)
+DECODE_TIE = 2e-4
+
+
+def _freq_gap(st, attended, cur):
+    """Relative gap between the last kept and the first dropped frequent
+    candidate of the oracle's decode step (policies.py:229-241 ranking)."""
+    import math
+
+    m = st.member
+    if st.scores is None or not (m.atoms & O.ATOM_FREQUENT) or (m.atoms & O.ATOM_FULL):
+        return np.inf
+    b = max(1, math.ceil(m.r_f * cur - 1e-9))
+    if b >= len(attended):
+        return np.inf
+    sc = st.scores[attended]
+    order = np.lexsort((attended, -sc))
+    hi, lo = sc[order[b - 1]], sc[order[b]]
+    return (hi - lo) / max(abs(hi), 1e-300)
+
+
 LARGE_BASE = 100000
+WIDE_BASE = 200000
 # AKV_FUZZ_SEEDS="a:b" widens the sweep (tools runs: profiles/r1_fuzz.md);
-# seeds >= LARGE_BASE draw prompts of 255-1500 positions
+# seeds >= LARGE_BASE draw prompts of 255-1500 positions, seeds >= WIDE_BASE
+# 128-768 heads per launch
 _rng = os.environ.get("AKV_FUZZ_SEEDS", "0:96").split(":")
 SEEDS = range(int(_rng[0]), int(_rng[1]))
 
@@ -121,15 +150,23 @@ def test_random_configuration_matches_oracle(seed):
     stats = {"max_rel_out_err": 0.0}
     # T = 1 puts every member that keeps all positions at R == T (rounding)
     assert c["T"] == 1.0 or len(keep) >= (G + 1) // 2, (seed, skip)
+    decode_ties = 0
     for t in range(D):
         pos = N + t
+        attended = {g: np.append(sess.heads[g].positions, pos) for g in keep}
         ref = O.decode_session_step(sess, c["q"][:, :, pos].astype(np.float64),
                                     c["k"][:, :, pos].astype(np.float64),
                                     c["v"][:, :, pos].astype(np.float64),
                                     c["cls"][:, pos].astype(np.int64))
-        for g in keep:
-            np.testing.assert_array_equal(np.flatnonzero(r["dec_kept"][t, g]),
-                                          np.sort(sess.heads[g].positions),
+        for g in list(keep):
+            got_kept = np.flatnonzero(r["dec_kept"][t, g])
+            want_kept = np.sort(sess.heads[g].positions)
+            if not np.array_equal(got_kept, want_kept) and \
+                    _freq_gap(sess.heads[g], attended[g], pos + 1) < DECODE_TIE:
+                keep.remove(g)   # a near tie at the frequent boundary: fp32 vs float64 order
+                decode_ties += 1
+                continue
+            np.testing.assert_array_equal(got_kept, want_kept,
                                           err_msg=f"seed {seed} step {t} head {g}")
         if not keep:   # T = 1: every head may sit at R == T
             break
@@ -145,7 +182,7 @@ def test_random_configuration_matches_oracle(seed):
         import json
 
         stats.update(seed=seed, dtype=c["dtype"], N=N, D=D, d=c["d"], G=G, T=c["T"],
-                     compared=len(keep), skipped=len(skip),
+                     compared=len(keep), skipped=len(skip), decode_ties=decode_ties,
                      head_steps=D * len(keep),
                      evict_steps=int(sum(1 for t in range(1, D) for g in keep
                                          if r["dec_kept"][t, g].sum() <= r["dec_kept"][t - 1, g].sum())))

@@ -21,7 +21,8 @@ def main():
     out = [f"# {tag}: randomised parity sweep, CUDA path vs the CPU oracle", "",
            "`tests/test_gpu_fuzz.py` widened with `AKV_FUZZ_SEEDS` on a B200 "
            "(`tools/fuzz_report.py`).  Seeds < 100000 draw prompts of 1-300 positions, "
-           "seeds >= 100000 of 255-1500 (multi-page segments); head dims 16-128, fp32/bf16, "
+           "seeds 100000-199999 of 255-1500 (multi-page segments), seeds >= 200000 batch 8-24 x "
+           "16-32 heads with prompts of 16-130; head dims 16-128, fp32/bf16, "
            "random family orders / drops, ratios, thresholds in [0, 1], planted biases, "
            "0-24 decode steps.  Bar per seed: policies and kept-index sets bit-exact after "
            "encode and after every decode step for every compared head; outputs within "
@@ -29,17 +30,20 @@ def main():
            "(near-T) or a frequent-boundary score gap < 1e-6 (near tie) are skipped, as the "
            "north star allows.", "",
            "| sweep | seeds | heads compared | heads skipped (near-T / near tie) | "
-           "decode head-steps compared | of which the head's live set did not grow | "
-           "max rel. output error fp32 / bf16 |", "|---|---:|---:|---:|---:|---:|---|"]
+           "heads stopped at a decode near tie | decode head-steps compared | "
+           "of which the head's live set did not grow | "
+           "max rel. output error fp32 / bf16 |", "|---|---:|---:|---:|---:|---:|---:|---|"]
     for name, sel in (("small (N <= 300)", lambda r: r["seed"] < 100000),
-                      ("large (N 255-1500)", lambda r: r["seed"] >= 100000)):
+                      ("large (N 255-1500)", lambda r: 100000 <= r["seed"] < 200000),
+                      ("wide (128-768 heads per launch)", lambda r: r["seed"] >= 200000)):
         rs = [r for r in rows if sel(r)]
         if not rs:
             continue
         e32 = max([r["max_rel_out_err"] for r in rs if r["dtype"] == "f32"] or [0])
         e16 = max([r["max_rel_out_err"] for r in rs if r["dtype"] == "bf16"] or [0])
         out.append(f"| {name} | {len(rs)} | {sum(r['compared'] for r in rs)} | "
-                   f"{sum(r['skipped'] for r in rs)} | {sum(r['head_steps'] for r in rs)} | "
+                   f"{sum(r['skipped'] for r in rs)} | {sum(r.get('decode_ties', 0) for r in rs)} | "
+                   f"{sum(r['head_steps'] for r in rs)} | "
                    f"{sum(r['evict_steps'] for r in rs)} | {e32:.1e} / {e16:.1e} |")
     t1 = [r for r in rows if r["T"] == 1.0]
     out += ["", f"Skipped heads concentrate at T = 1 ({sum(r['skipped'] for r in t1)} of "
