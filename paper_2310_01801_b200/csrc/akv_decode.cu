@@ -1201,10 +1201,14 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
 #pragma unroll
       for (int t = 0; t < TILES; ++t) {
         const int r0 = wrow0 + t * 16;
-        // p in bf16, packed (key gq | key gq+8) on the owning lanes
-        const __nv_bfloat16 p0 = __float2bfloat16_rn(sx[t][0] == -INFINITY ? 0.f : __expf(sx[t][0] - m_new));
-        const __nv_bfloat16 p1 = __float2bfloat16_rn(sx[t][1] == -INFINITY ? 0.f : __expf(sx[t][1] - m_new));
-        if (qq == 0) l_run += __bfloat162float(p0) + __bfloat162float(p1);
+        // p in bf16 for the PV product, packed (key gq | key gq+8) on the
+        // owning lanes; the softmax sum takes the fp32 values, so the lse the
+        // score update divides by carries fp32 (not bf16) rounding
+        const float e0 = sx[t][0] == -INFINITY ? 0.f : __expf(sx[t][0] - m_new);
+        const float e1 = sx[t][1] == -INFINITY ? 0.f : __expf(sx[t][1] - m_new);
+        const __nv_bfloat16 p0 = __float2bfloat16_rn(e0);
+        const __nv_bfloat16 p1 = __float2bfloat16_rn(e1);
+        if (qq == 0) l_run += e0 + e1;
         const uint32_t pk = (uint32_t)__bfloat16_as_ushort(p0) | ((uint32_t)__bfloat16_as_ushort(p1) << 16);
         const uint32_t u = __shfl_sync(0xffffffffu, pk, 8 * qq);      // keys 2qq, 2qq+8
         const uint32_t v = __shfl_sync(0xffffffffu, pk, 8 * qq + 4);  // keys 2qq+1, 2qq+9
