@@ -267,6 +267,14 @@ __device__ void block_topk_threshold(int n, int k, Get get, int* hist, int* red,
   *thr_pos = kPosMask - s_pprefix;
 }
 
+// Radix key of a (finite, >= 0) float64 score: its bit pattern, which orders
+// like the value.  -0.0 is folded onto +0.0 first (the reference's stable
+// argsort ties them, policies.py:238-240; their raw bits would rank -0.0
+// above every positive score).
+__device__ __forceinline__ unsigned long long score_key(double s) {
+  return (unsigned long long)__double_as_longlong(__dadd_rn(s, 0.0));
+}
+
 __device__ __forceinline__ bool topk_selected(unsigned long long key, int pos,
                                               unsigned long long thr_key, int thr_pos) {
   return key > thr_key || (key == thr_key && pos <= thr_pos);

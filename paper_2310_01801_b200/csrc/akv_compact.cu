@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(128) k2_compact(CompactParams p) {
     const int pos = kp[i0 + r];
     const int64_t slot = base + i0 + r;
     const double sc = freq ? p.colsum[(size_t)g * p.N + pos] : 0.0;
-    const bool inF = freq && topk_selected((unsigned long long)__double_as_longlong(sc), pos,
+    const bool inF = freq && topk_selected(score_key(sc), pos,
                                            p.thr_key[g], p.thr_pos[g]);
     p.meta[slot] = pos | ((int)p.cls[(size_t)b * p.cls_ld + pos] << kClsShift) | (inF ? kInF : 0);
     p.score[slot] = sc;

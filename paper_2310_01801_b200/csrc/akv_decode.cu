@@ -192,7 +192,12 @@ __device__ __forceinline__ long long plan_pages_bound(const DecParams& p, int pa
   const int lo = min(G, (int)threadIdx.x * per), hi = min(G, lo + per);
   int cnt = 0;
   for (int g = lo; g < hi; ++g) {
-    const int bound = min(p.base_live[g] + step, p.seg_cap[g] - 1);
+    const int want = p.base_live[g] + step;
+    // a full-cache head's live count is exactly base_live + step: past its
+    // segment the insert cannot fit (flag it; writes stay in bounds)
+    if (want > p.seg_cap[g] - 1 && (p.atoms[g] & AKV_ATOM_FULL) && blockIdx.x == 0)
+      atomicExch(p.status, AKV_ERR_CAPACITY);
+    const int bound = min(want, p.seg_cap[g] - 1);
     s_live[g] = bound;
     s_full[g] = (p.atoms[g] & AKV_ATOM_FULL) ? 1 : 0;
     cnt += (bound + 1 + page - 1) / page;
@@ -295,7 +300,7 @@ __device__ void policy_v3(const DecParams& p, const HeadCtx& hc, float lse, int*
       if (j == L) new_ck = ck;
       else if (!ck && !inF) { ++nk_cnt; nk_min = min(nk_min, j); nk_max = max(nk_max, j); }
       if (freq) {
-        const unsigned long long key = (unsigned long long)__double_as_longlong(sv[i]);
+        const unsigned long long key = score_key(sv[i]);
         const int ps = meta_pos(mv[i]);
         if (inF) {
           ++cntF;
@@ -425,7 +430,7 @@ __device__ void policy_v3(const DecParams& p, const HeadCtx& hc, float lse, int*
         for (int i = 0; i < kEpr; ++i) {
           const int j = b0 + i * NC + tid;
           if (j >= n) continue;
-          const unsigned long long key = (unsigned long long)__double_as_longlong(sv[i]);
+          const unsigned long long key = score_key(sv[i]);
           const int ps = meta_pos(mv[i]);
           if (above(key, ps, mn, mnp)) { my_above += (mv[i] & kInF) ? 1 : 0; continue; }
           if (above(mf, mfp, key, ps)) continue;  // strictly below the weakest F member
@@ -454,13 +459,13 @@ __device__ void policy_v3(const DecParams& p, const HeadCtx& hc, float lse, int*
       unsigned long long thr_key;
       int thr_pos;
       auto get = [&](int i, unsigned long long* key, int* pos) {
-        *key = (unsigned long long)__double_as_longlong(__ldcg(score + i));
+        *key = score_key(__ldcg(score + i));
         *pos = meta_pos(__ldcg(meta + i));
       };
       block_topk_threshold<CS>(n, s_kb, get, hist, red_i, &thr_key, &thr_pos);
       for (int j = tid; j < n; j += NC) {
         const int m = __ldcg(meta + j);
-        const bool sel = topk_selected((unsigned long long)__double_as_longlong(__ldcg(score + j)),
+        const bool sel = topk_selected(score_key(__ldcg(score + j)),
                                        meta_pos(m), thr_key, thr_pos);
         const int nm = sel ? (m | kInF) : (m & ~kInF);
         if (nm != m) meta[j] = nm;
@@ -1242,6 +1247,11 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
       // consumer warps, in parallel with the epilogue warps finishing the
       // previous segment (that serialisation was the step's tail).  Every
       // page has been consumed, so stage 0 holds the handoff scratch.
+      // The split-K partials, semaphore, output and live counts belong to
+      // the previous step until it completes: a chained step whose pages
+      // all streamed early waits for it here (the head's other parts may
+      // sit in CTAs whose producer never had to wait).
+      if (early) grid_dep_wait();
       using CSync = NamedSync<NW * 32, 3, 0>;
       CSync::sync();  // all consumer warps are past the last page
       float(*red)[D] = reinterpret_cast<float(*)[D]>(smem);
@@ -1290,47 +1300,51 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
 }
 
 // ===========================================================================
-static int g_num_sms = 0;
+// Tuning knobs read from the environment once per process (thread-safe
+// static initialisation).
+static int env_int(const char* name, int dflt) {
+  const char* s = getenv(name);
+  return s ? atoi(s) : dflt;
+}
 // Decode grid: AKV_K3_GRID CTAs if set (tuning), else 2 per SM
 static int k3_grid(int sms) {
-  static int v = -1;
-  if (v < 0) {
-    const char* s = getenv("AKV_K3_GRID");
-    v = s ? atoi(s) : 0;
-  }
+  static const int v = env_int("AKV_K3_GRID", 0);
   return v > 0 ? v : 2 * sms;
 }
 unsigned long long* g_dec_trace = nullptr;  // set by akv_debug_set_decode_trace
 // consumers publish the CTA's last full-cache segment (AKV_K3_CONSUMER_TAIL, tuning)
 static int k3_consumer_tail() {
-  static int v = -1;
-  if (v < 0) {
-    const char* s = getenv("AKV_K3_CONSUMER_TAIL");
-    v = s ? atoi(s) != 0 : 1;
-  }
+  static const int v = env_int("AKV_K3_CONSUMER_TAIL", 1) != 0;
   return v;
 }
 // pages of L2 prefetch ahead of the ring (AKV_K3_L2_PREFETCH, tuning)
 static int k3_l2_prefetch() {
-  static int v = -1;
-  if (v < 0) {
-    const char* s = getenv("AKV_K3_L2_PREFETCH");
-    v = s ? atoi(s) : 0;  // measured at config 1: 0 best (2: +0.6 us, 4: +1.4, 8: +4.1)
-    if (v < 0) v = 0;
-  }
+  // measured at config 1: 0 best (2: +0.6 us, 4: +1.4, 8: +4.1)
+  static const int v = env_int("AKV_K3_L2_PREFETCH", 0) > 0 ? env_int("AKV_K3_L2_PREFETCH", 0) : 0;
   return v;
 }
 
-static cudaError_t num_sms(int* out) {
-  if (!g_num_sms) {
-    int dev;
-    cudaError_t e;
-    if ((e = cudaGetDevice(&dev))) return e;
-    if ((e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev))) return e;
+static std::atomic<int> g_num_sms[kMaxDevices];
+
+}  // namespace akv
+
+cudaError_t akv::current_sm_count(int* out) {
+  int dev;
+  cudaError_t e;
+  if ((e = cudaGetDevice(&dev))) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  int v = g_num_sms[dev].load(std::memory_order_relaxed);
+  if (!v) {
+    if ((e = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev))) return e;
+    g_num_sms[dev].store(v, std::memory_order_relaxed);
   }
-  *out = g_num_sms;
+  *out = v;
   return cudaSuccess;
 }
+
+namespace akv {
+
+static cudaError_t num_sms(int* out) { return current_sm_count(out); }
 
 // Launch with programmatic dependent launch: the next step's CTAs start
 // their prologue while this step drains (griddepcontrol in the kernels).
@@ -1354,14 +1368,12 @@ template <typename T, int D>
 static cudaError_t launch_simt(const DecParams& p, cudaStream_t st) {
   using S = SimtShape<T, D>;
   auto kern = k3_decode_simt<T, D>;
-  static bool attr = false;
-  cudaError_t e;
-  if (!attr) {
-    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(kStages * S::STAGE_B + (2 * kMaxHeads + 1) * 4))))
-      return e;
-    attr = true;
-  }
+  static PerDeviceOnce attr;
+  cudaError_t e = attr.run([&](int) {
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(kStages * S::STAGE_B + (2 * kMaxHeads + 1) * 4));
+  });
+  if (e != cudaSuccess) return e;
   int sms;
   if ((e = num_sms(&sms))) return e;
   const size_t smem = (size_t)kStages * S::STAGE_B + (size_t)(2 * p.G + 1) * 4;
@@ -1405,28 +1417,34 @@ static cudaError_t launch_mma(const DecParams& p, int64_t total_slots, cudaStrea
   auto k3 = k3_decode_mma<D, 3>;
   auto k2 = k3_decode_mma<D, 2>;
   const size_t plan = (size_t)(2 * kMaxHeads + 1) * 4 + kMaxHeads;
-  static bool attr = false;
-  static size_t static3 = 0, static2 = 0, per_sm = 0, reserve = 0;
-  cudaError_t e;
-  if (!attr) {
-    if ((e = cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  // per-device launch facts: the attribute opt-ins and the shared-memory
+  // budget that decides whether a 3-stage ring keeps two CTAs per SM
+  struct Facts { size_t static3, per_sm, reserve; };
+  static Facts facts[kMaxDevices];
+  static PerDeviceOnce attr;
+  cudaError_t e = attr.run([&](int dev) {
+    cudaError_t r;
+    if ((r = cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(1024 + 3 * S::STAGE_B + plan))) ||
-        (e = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        (r = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(1024 + 2 * S::STAGE_B + plan))))
-      return e;
+      return r;
     cudaFuncAttributes fa;
-    if ((e = cudaFuncGetAttributes(&fa, k3))) return e;
-    static3 = fa.sharedSizeBytes;
-    if ((e = cudaFuncGetAttributes(&fa, k2))) return e;
-    static2 = fa.sharedSizeBytes;
-    int dev = 0, v = 0;
-    if ((e = cudaGetDevice(&dev))) return e;
-    if ((e = cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev))) return e;
-    per_sm = (size_t)v;
-    if ((e = cudaDeviceGetAttribute(&v, cudaDevAttrReservedSharedMemoryPerBlock, dev))) return e;
-    reserve = (size_t)v;
-    attr = true;
-  }
+    if ((r = cudaFuncGetAttributes(&fa, k3))) return r;
+    Facts f;
+    f.static3 = fa.sharedSizeBytes;
+    int v = 0;
+    if ((r = cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev))) return r;
+    f.per_sm = (size_t)v;
+    if ((r = cudaDeviceGetAttribute(&v, cudaDevAttrReservedSharedMemoryPerBlock, dev))) return r;
+    f.reserve = (size_t)v;
+    facts[dev] = f;
+    return cudaSuccess;
+  });
+  if (e != cudaSuccess) return e;
+  int dev = 0;
+  if ((e = cudaGetDevice(&dev))) return e;
+  const Facts& f = facts[dev];
   int sms;
   if ((e = num_sms(&sms))) return e;
   const size_t plan_g = (size_t)(2 * p.G + 1) * 4 + p.G;
@@ -1436,15 +1454,10 @@ static cudaError_t launch_mma(const DecParams& p, int64_t total_slots, cudaStrea
   // CTAs per SM up to 2048 heads per launch, where a 3-stage ring drops to
   // one CTA per SM beyond 512 heads (3.5 vs 5.9 TB/s).  AKV_K3_STAGES=3
   // selects the 3-stage ring where two CTAs still fit (tuning).
-  static int stages = -1;
-  if (stages < 0) {
-    const char* fs = getenv("AKV_K3_STAGES");
-    stages = fs ? atoi(fs) : 2;
-  }
-  if (stages == 3 && 2 * (smem3 + static3 + reserve) <= per_sm)
+  static const int stages = env_int("AKV_K3_STAGES", 2);
+  if (stages == 3 && 2 * (smem3 + f.static3 + f.reserve) <= f.per_sm)
     return launch_pdl(k3, k3_grid(sms), S::THREADS, smem3, st, p, tm->k, tm->v);
   const size_t smem2 = 1024 + (size_t)2 * S::STAGE_B + plan_g;
-  (void)static2;
   return launch_pdl(k2, k3_grid(sms), S::THREADS, smem2, st, p, tm->k, tm->v);
 }
 
@@ -1507,8 +1520,8 @@ extern "C" int akv_decode_workspace_init(void* ws, size_t bytes, int32_t B, int3
 extern "C" int akv_decode_step(const akv_decode_args* a, void* stream) {
   if (!a) return set_error(AKV_ERR_INVALID, "akv_decode_step: null args");
   if (a->B < 1 || a->H < 1) return set_error(AKV_ERR_INVALID, "akv_decode_step: empty input");
-  if (a->B * a->H > kMaxHeads)
-    return set_error(AKV_ERR_UNSUPPORTED, "akv_decode_step: more than %d heads per launch", kMaxHeads);
+  if (a->H > kMaxHeads)
+    return set_error(AKV_ERR_UNSUPPORTED, "akv_decode_step: more than %d heads per batch row", kMaxHeads);
   if ((!a->pos_dev && a->pos < a->prompt_len) || a->prompt_len < 1)
     return set_error(AKV_ERR_INVALID, "akv_decode_step: need pos >= prompt_len >= 1");
   if (a->pos_dev && (a->flags & AKV_DECODE_CHAINED))
@@ -1523,36 +1536,54 @@ extern "C" int akv_decode_step(const akv_decode_args* a, void* stream) {
                      a->n_peers, (long long)a->peer_ld);
   DecWs w = carve(a->workspace_dev, a->B, a->H, a->d, a->max_cap, a->total_slots);
   if (a->workspace_bytes < w.bytes) return set_error(AKV_ERR_CAPACITY, "akv_decode_step: workspace too small");
-  DecParams p{a->B, a->H, a->B * a->H, a->prompt_len, a->pos, a->q_dev, a->k_dev, a->v_dev,
-              a->bh_stride, a->new_cls_dev, a->slope_dev, a->sink_dev, a->head_atoms_dev,
-              a->head_r_l_dev, a->head_r_f_dev, a->seg_off_dev, a->seg_cap_dev, a->kc_dev, a->vc_dev,
-              a->meta_dev, a->score_dev, a->base_live_dev, a->live_in_dev, a->live_out_dev,
-              a->out_dev,
-              a->evicted_dev, a->status_dev ? a->status_dev : w.status, w.part, w.logit, w.counter,
-              w.max_parts, (float)(1.0 / sqrt((double)a->d)), g_dec_trace, a->pos_dev, a->flags,
-              a->lse_out_dev, a->peer_out_dev, a->n_peers, a->peer_ld, a->peer_col0,
-              a->dtype == AKV_DTYPE_BF16, k3_l2_prefetch(), k3_consumer_tail()};
+  const float scale = (float)(1.0 / sqrt((double)a->d));
+  const size_t es = a->dtype == AKV_DTYPE_BF16 ? 2 : 4;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaErrorInvalidValue;
+  cudaError_t e = cudaSuccess;
   bool ok = true;
-  if (a->dtype == AKV_DTYPE_BF16) {
-    switch (a->d) {
-      case 16: e = launch_simt<__nv_bfloat16, 16>(p, st); break;
-      case 32: e = launch_simt<__nv_bfloat16, 32>(p, st); break;
-      case 64: e = g_disable_tc ? launch_simt<__nv_bfloat16, 64>(p, st) : launch_mma<64>(p, a->total_slots, st); break;
-      case 128: e = g_disable_tc ? launch_simt<__nv_bfloat16, 128>(p, st) : launch_mma<128>(p, a->total_slots, st); break;
-      default: ok = false;
+  // Heads are independent: batches beyond kMaxHeads heads per launch (the
+  // page plan lives in shared memory) run as consecutive launches over
+  // whole batch rows.  Each launch depends programmatically only on the one
+  // before it, and every launch's CTAs wait for their predecessor before
+  // signalling, so the chained-step invariant (only the immediately
+  // preceding launch may still be writing) holds for every chunk.
+  const int rows_per = kMaxHeads / a->H;
+  for (int b0 = 0; b0 < a->B && ok && e == cudaSuccess; b0 += rows_per) {
+    const int nb = min(rows_per, a->B - b0);
+    const int64_t g0 = (int64_t)b0 * a->H;
+    const int64_t qoff = g0 * a->bh_stride * (int64_t)es;
+    auto at = [&](auto* ptr, int64_t n) { return ptr ? ptr + n : ptr; };
+    DecParams p{nb, a->H, nb * a->H, a->prompt_len, a->pos,
+                static_cast<const char*>(a->q_dev) + qoff, static_cast<const char*>(a->k_dev) + qoff,
+                static_cast<const char*>(a->v_dev) + qoff, a->bh_stride, a->new_cls_dev + b0,
+                a->slope_dev, a->sink_dev, a->head_atoms_dev + g0, a->head_r_l_dev + g0,
+                a->head_r_f_dev + g0, a->seg_off_dev + g0, a->seg_cap_dev + g0, a->kc_dev, a->vc_dev,
+                a->meta_dev, a->score_dev, a->base_live_dev + g0, a->live_in_dev + g0,
+                a->live_out_dev + g0, a->out_dev + g0 * a->d, at(a->evicted_dev, g0),
+                a->status_dev ? a->status_dev : w.status,
+                w.part + g0 * w.max_parts * (a->d + 2), w.logit, w.counter + g0, w.max_parts, scale,
+                g_dec_trace, a->pos_dev, a->flags, at(a->lse_out_dev, g0), a->peer_out_dev,
+                a->n_peers, a->peer_ld, a->peer_col0 + (int64_t)b0 * a->peer_ld,
+                a->dtype == AKV_DTYPE_BF16, k3_l2_prefetch(), k3_consumer_tail()};
+    if (a->dtype == AKV_DTYPE_BF16) {
+      switch (a->d) {
+        case 16: e = launch_simt<__nv_bfloat16, 16>(p, st); break;
+        case 32: e = launch_simt<__nv_bfloat16, 32>(p, st); break;
+        case 64: e = g_disable_tc ? launch_simt<__nv_bfloat16, 64>(p, st) : launch_mma<64>(p, a->total_slots, st); break;
+        case 128: e = g_disable_tc ? launch_simt<__nv_bfloat16, 128>(p, st) : launch_mma<128>(p, a->total_slots, st); break;
+        default: ok = false;
+      }
+    } else if (a->dtype == AKV_DTYPE_F32) {
+      switch (a->d) {
+        case 16: e = launch_simt<float, 16>(p, st); break;
+        case 32: e = launch_simt<float, 32>(p, st); break;
+        case 64: e = launch_simt<float, 64>(p, st); break;
+        case 128: e = launch_simt<float, 128>(p, st); break;
+        default: ok = false;
+      }
+    } else {
+      ok = false;
     }
-  } else if (a->dtype == AKV_DTYPE_F32) {
-    switch (a->d) {
-      case 16: e = launch_simt<float, 16>(p, st); break;
-      case 32: e = launch_simt<float, 32>(p, st); break;
-      case 64: e = launch_simt<float, 64>(p, st); break;
-      case 128: e = launch_simt<float, 128>(p, st); break;
-      default: ok = false;
-    }
-  } else {
-    ok = false;
   }
   if (!ok) return set_error(AKV_ERR_UNSUPPORTED, "akv_decode_step: unsupported dtype %d / head dim %d", a->dtype, a->d);
   if (e != cudaSuccess) return set_error(AKV_ERR_CUDA, "akv_decode_step: %s", cudaGetErrorString(e));

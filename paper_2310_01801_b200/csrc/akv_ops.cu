@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kOpsThreads) ops_keep_mask(KeepParams p) {
     const int kb = budget(p.r_f[g], cur);
     auto get = [&](int i, unsigned long long* key, int* pos) {
       const int j = list[i];
-      *key = (unsigned long long)__double_as_longlong(sc[j]);
+      *key = score_key(sc[j]);
       *pos = j;
     };
     block_topk_threshold(total, kb, get, hist, red, &tk, &tp);
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kOpsThreads) ops_keep_mask(KeepParams p) {
       k |= (at & AKV_ATOM_SPECIAL) && c == AKV_CLS_SPECIAL;
       k |= (at & AKV_ATOM_PUNCT) && c == AKV_CLS_PUNCT;
       k |= (at & AKV_ATOM_LOCAL) && j >= ws;
-      if (freq) k |= topk_selected((unsigned long long)__double_as_longlong(sc[j]), j, tk, tp);
+      if (freq) k |= topk_selected(score_key(sc[j]), j, tk, tp);
     }
     keep[j] = k;
     cnt += k;

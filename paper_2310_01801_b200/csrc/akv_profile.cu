@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kPolicyThreads) k1_policy(PolicyParams p) {
   const float* lastp = p.lastp + (size_t)g * N;
 
   auto get = [&](int i, unsigned long long* key, int* pos) {
-    *key = __double_as_longlong(colsum[i]);
+    *key = score_key(colsum[i]);
     *pos = i;
   };
   // exact frequent top-k thresholds (one per member with FREQUENT), and the
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(kPolicyThreads) k1_policy(PolicyParams p) {
     if (kb < N) {
       unsigned long long nk = 0ull;
       for (int j = threadIdx.x; j < N; j += blockDim.x) {
-        const unsigned long long key = __double_as_longlong(colsum[j]);
+        const unsigned long long key = score_key(colsum[j]);
         if (!topk_selected(key, j, tk, tp) && key > nk) nk = key;
       }
 #pragma unroll
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kPolicyThreads) k1_policy(PolicyParams p) {
              ((at & AKV_ATOM_PUNCT) && c == AKV_CLS_PUNCT);
     if (at & AKV_ATOM_LOCAL) k |= j >= N - budget(p.r_l[f], p.local_len);
     if (at & AKV_ATOM_FREQUENT)
-      k |= topk_selected(__double_as_longlong(colsum[j]), j, s_thr_key[f], s_thr_pos[f]);
+      k |= topk_selected(score_key(colsum[j]), j, s_thr_key[f], s_thr_pos[f]);
     return k;
   };
 

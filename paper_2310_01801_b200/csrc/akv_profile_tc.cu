@@ -542,15 +542,15 @@ cudaError_t launch_tc_passes(const void* q, const void* k, const void* v, int B,
   if (!encode_tmap_2d_bf16(&tmQ, q, rows, 128, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !encode_tmap_2d_bf16(&tmK, k, rows, 128, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
-  static bool attr = false;
-  cudaError_t e;
-  if (!attr) {
-    if ((e = cudaFuncSetAttribute(k1tc_rowlse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem)))
-      return e;
-    if ((e = cudaFuncSetAttribute(k1tc_colsum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem)))
-      return e;
-    attr = true;
-  }
+  static PerDeviceOnce attr;
+  cudaError_t e = attr.run([](int) {
+    cudaError_t r = cudaFuncSetAttribute(k1tc_rowlse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kTcSmem);
+    if (r == cudaSuccess)
+      r = cudaFuncSetAttribute(k1tc_colsum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
+    return r;
+  });
+  if (e != cudaSuccess) return e;
   TcParams p{H, N, ld, cls, cls_ld, slope, sink, static_cast<const __nv_bfloat16*>(v), lse, colsum,
              colsq, lastp, out_part, (float)(1.0 / sqrt(128.0))};
   const dim3 grid(tc_tiles(N), G);

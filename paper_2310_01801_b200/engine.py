@@ -183,8 +183,10 @@ class CompressedCache:
 
     @property
     def pending_output(self) -> torch.Tensor:
-        """Latest attention output per head, fp32 [B, H, d]."""
-        return self.out
+        """Latest attention output per head, fp32 [B, H, d]: the buffer the
+        last decode step wrote (its ``out=`` argument when one was given)."""
+        latest = getattr(self, "_latest_out", None)
+        return self.out if latest is None else latest
 
     @property
     def heads(self) -> dict:
@@ -204,7 +206,7 @@ class CompressedCache:
         kc = self.kc.float().cpu().numpy()
         vc = self.vc.float().cpu().numpy()
         score = self.score.cpu().numpy()
-        out = self.out.reshape(self.G, -1).double().cpu().numpy()
+        out = self.pending_output.reshape(self.G, -1).double().cpu().numpy()
         rec = self.step_recovery.cpu().numpy()
         atoms = self.head_atoms.cpu().numpy()
         fam = self.profile_result.family if self.profile_result is not None else ()
@@ -655,6 +657,7 @@ def decode_step_tensors(cache: CompressedCache, q, k, v, new_classes, out=None, 
     check(lib.akv_decode_step(C.byref(a), _stream()), EngineError)
     cache._parity ^= 1
     cache.seq_len += 1
+    cache._latest_out = dst
     return dst
 
 
@@ -677,6 +680,7 @@ def decode_step_launch(cache: CompressedCache, q, k, v, new_classes, out, parity
     if cache.track_recovery:
         _launch_recovery(cache, q, k, new_classes, cache.live_buf[parity], pos_dev=pos_dev)
     check(lib.akv_decode_step(C.byref(a), _stream()), EngineError)
+    cache._latest_out = out
     return out
 
 
@@ -816,7 +820,7 @@ def generate_step(model, cache: CompressedCache, last_token=None, sampler=None):
             grow_cache(cache, max(cache.capacity_steps, 16))
         decode_step_tensors(cache, qd.to(cache.dtype), kd.to(cache.dtype), vd.to(cache.dtype),
                             cache._model_new_cls)
-    concat = cache.out.reshape(-1).double().cpu().numpy()
+    concat = cache.pending_output.reshape(-1).double().cpu().numpy()
     next_token = sampler(model.head_logits(concat))
     live = cache.head_retained()
     cache.last_record = StepRecord(

@@ -65,8 +65,61 @@ def test_exp_roofline():
     assert abs(r["peak"] - 16 * sms * 1000e6 / 1e9) < 1e-6
 
 
-def test_oracle_leg_runs_on_a_tiny_workload():
+def test_cpu_legs_run_on_a_tiny_workload():
     import bench
 
-    secs = bench._oracle_heads((1, 0, [0, 1], 0.95, 1, 2, 16, 2))
-    assert secs > 0
+    for kind in ("port", "reference"):
+        if kind == "reference" and not bench._reference_available():
+            continue
+        secs = bench._cpu_job((1, [(0, [0, 1])], 0.95, 1, 2, 16, 2, kind))
+        assert secs > 0
+
+
+def test_reference_arm_does_not_map_the_product_library():
+    """The CPU legs load the workload generator by path: the product
+    package (whose import maps libakv_sm100a.so) stays unimported."""
+    import subprocess
+    import sys
+
+    import bench
+
+    code = ("import sys, bench; bench._cpu_job((1, [(0, [0])], 0.95, 1, 2, 16, 2, bench._cpu_kind())); "
+            "assert 'paper_2310_01801_b200' not in sys.modules, 'product package imported'; "
+            "maps = open('/proc/self/maps').read(); assert 'libakv_sm100a' not in maps; print('ok')")
+    r = subprocess.run([sys.executable, "-c", code], cwd=bench.ROOT, capture_output=True, text=True)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_reference_leg_matches_the_oracle_port_on_a_small_session():
+    """The folded model drives the unmodified reference to the same kept
+    sets the oracle port computes (planted sink head, evictions)."""
+    import bench
+
+    if not bench._reference_available():
+        import pytest
+
+        pytest.skip("baseline/_ref not installed")
+    import numpy as np
+    from adaptive_kv import ProfilerConfig, encode_prompt, generate_step
+
+    from oracle import akv_oracle as O
+
+    W = bench._workloads()
+    w = W.config1(seed=1, B=1, H=32, N=96, D=6)
+    heads = [h for h in range(w.H) if w.sinks[h]][:2] + [0]
+    m = bench._FoldedModel(w, 0, heads)
+    N = w.N
+    _, cache = encode_prompt(m, [int(x) for x in m.tokens[:N]], ProfilerConfig(recovery_threshold=0.99),
+                             diagnostics=False)
+    generate_step(m, cache, None)
+    for t in range(w.D):
+        generate_step(m, cache, int(m.tokens[N + t]))
+    cls = W.class_lut()[w.tokens(0)].astype(np.int64)
+    fam = O.default_family(w.r_l, w.r_f)
+    for i, h in enumerate(heads):
+        q, k, v = (x.astype(np.float64) for x in w.head_qkv(0, h))
+        prof = O.profile_head(q[:N], k[:N], v[:N], cls, w.slopes[h], w.sinks[h], fam, [0.99])
+        st = O.compact_head(prof, k[:N], v[:N], fam[prof.choice[0]], N, w.slopes[h], w.sinks[h])
+        for t in range(w.D):
+            O.decode_head(st, q[N + t], k[N + t], v[N + t], N + t, cls, N)
+        assert list(np.sort(st.positions)) == cache.heads[(0, i)].positions

@@ -1,0 +1,116 @@
+"""K3 launch-level invariants on the B200, through the C-ABI:
+
+* chained steps (AKV_DECODE_CHAINED: a step streams settled full-cache
+  pages while its predecessor drains, programmatic dependent launch) give
+  bit-identical outputs and kept sets to unchained steps - with few heads
+  per launch, so a head's pages split over several CTAs and the consumer
+  warps publish split-K partials while the previous step may still run;
+* batches beyond the 2,048 heads one launch plans for run as consecutive
+  launches over batch rows, bit-identical to running the rows separately,
+  and match the CPU oracle (engine.py:303-350).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import NAME_BIT  # noqa: F401  (puts the oracle on the path)
+from oracle import akv_oracle as O
+from paper_2310_01801_b200 import ProfilerConfig, decode_step_tensors, encode_prompt_tensors
+from paper_2310_01801_b200.workloads import Workload, class_lut
+
+pytestmark = pytest.mark.gpu
+
+
+def _workload(B, H, N, D, d, seed):
+    rng = np.random.default_rng([seed, 99])
+    sinks = np.where(rng.random(H) < 0.6, rng.uniform(7.0, 11.0, H), 0.0)
+    slopes = np.where(rng.random(H) < 0.3, 0.05, 0.0)
+    return Workload("chain", B, H, N, D, d, "bf16", (0.99,), seed=seed, slopes=slopes,
+                    sinks=sinks)
+
+
+def _inputs(w, rows=None):
+    rows = list(range(w.B)) if rows is None else rows
+    dev = torch.device("cuda")
+    q = np.stack([np.stack([w.head_qkv(b, h)[0] for h in range(w.H)]) for b in rows])
+    k = np.stack([np.stack([w.head_qkv(b, h)[1] for h in range(w.H)]) for b in rows])
+    v = np.stack([np.stack([w.head_qkv(b, h)[2] for h in range(w.H)]) for b in rows])
+    cls = class_lut()[np.stack([w.tokens(b) for b in rows])]
+    t = lambda x: torch.from_numpy(x).to(dev).to(torch.bfloat16)
+    return t(q), t(k), t(v), torch.from_numpy(cls).to(dev)
+
+
+def _session(w, T, chained, rows=None, kept_every=1):
+    qd, kd, vd, cd = _inputs(w, rows)
+    dev = qd.device
+    sl = torch.tensor(w.slopes, dtype=torch.float32, device=dev)
+    sk = torch.tensor(w.sinks, dtype=torch.float32, device=dev)
+    res, cache = encode_prompt_tensors(qd, kd, vd, cd, ProfilerConfig(recovery_threshold=T),
+                                       prompt_len=w.N, max_new_tokens=w.D, slopes=sl, sinks=sk)
+    G = qd.shape[0] * w.H
+    outs = torch.empty(w.D, G, w.d, dtype=torch.float32, device=dev)
+    kept = []
+    cols = [cd[:, w.N + t].contiguous() for t in range(w.D)]
+    for t in range(w.D):
+        p = w.N + t
+        decode_step_tensors(cache, qd[:, :, p], kd[:, :, p], vd[:, :, p], cols[t],
+                            out=outs[t].view(-1, w.H, w.d), chained=chained)
+        if (t + 1) % kept_every == 0 or t + 1 == w.D:
+            kept.append(cache.retained_positions())
+    torch.cuda.synchronize()
+    cache.check()
+    return res, outs.cpu().numpy(), kept
+
+
+@pytest.mark.parametrize("d,H", [(128, 4), (128, 12), (64, 6)])
+def test_chained_steps_bit_identical(d, H):
+    w = _workload(1, H, 700, 96, d, seed=5 + d + H)
+    r0, o0, k0 = _session(w, 0.99, chained=False)
+    r1, o1, k1 = _session(w, 0.99, chained=True)
+    np.testing.assert_array_equal(r0.choice, r1.choice)
+    assert not all(r0.family[c].is_full for c in r0.choice[:, 0]), "every head full: no eviction"
+    np.testing.assert_array_equal(o0, o1)
+    for t, (a, b) in enumerate(zip(k0, k1)):
+        for g, (x, y) in enumerate(zip(a, b)):
+            np.testing.assert_array_equal(x, y, err_msg=f"step {t} head {g}")
+
+
+def test_more_than_2048_heads_per_call():
+    """B=72 x H=32 = 2,304 heads: two launches per step (64 + 8 rows)."""
+    w = _workload(72, 32, 160, 24, 128, seed=11)
+    r, o, k = _session(w, 0.99, chained=True, kept_every=8)
+    ra, oa, ka = _session(w, 0.99, chained=True, rows=list(range(64)), kept_every=8)
+    rb, ob, kb = _session(w, 0.99, chained=True, rows=list(range(64, 72)), kept_every=8)
+    G1 = 64 * w.H
+    np.testing.assert_array_equal(r.choice[:G1], ra.choice)
+    np.testing.assert_array_equal(r.choice[G1:], rb.choice)
+    np.testing.assert_array_equal(o[:, :G1], oa)
+    np.testing.assert_array_equal(o[:, G1:], ob)
+    for s in range(len(k)):
+        for g in range(w.B * w.H):
+            ref = ka[s][g] if g < G1 else kb[s][g - G1]
+            np.testing.assert_array_equal(k[s][g], ref)
+    # oracle on heads of both launches
+    lut = class_lut()
+    fam = O.default_family(w.r_l, w.r_f)
+    for b, h in [(0, 1), (63, 30), (64, 2), (71, 31), (70, 5)]:
+        g = b * w.H + h
+        cls = lut[w.tokens(b)].astype(np.int64)
+        q, kk, v = (x.astype(np.float64) for x in w.head_qkv(b, h))
+        N = w.N
+        prof = O.profile_head(q[:N], kk[:N], v[:N], cls, w.slopes[h], w.sinks[h], fam, [0.99])
+        assert int(r.choice[g, 0]) == int(prof.choice[0]) or \
+            np.any(np.abs(prof.recoveries[:max(int(prof.choice[0]), int(r.choice[g, 0])) + 1] - 0.99) < 1e-4)
+        if int(r.choice[g, 0]) != int(prof.choice[0]):
+            continue
+        st = O.compact_head(prof, kk[:N], v[:N], fam[prof.choice[0]], N, w.slopes[h], w.sinks[h])
+        si = 0
+        for t in range(w.D):
+            out = O.decode_head(st, q[N + t], kk[N + t], v[N + t], N + t, cls, N)
+            sc = np.abs(out).max()
+            np.testing.assert_allclose(o[t, g], out, rtol=2e-2, atol=2e-2 * sc)
+            if (t + 1) % 8 == 0 or t + 1 == w.D:
+                np.testing.assert_array_equal(k[si][g], np.sort(st.positions),
+                                              err_msg=f"head {g} step {t}")
+                si += 1
