@@ -15,8 +15,14 @@ every decode step (~130-200 MB) is larger than the 126 MB L2.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-Under torchrun every rank runs its own c1 batch (seed offset by rank; weak
-scaling, no data-path collective); rank 0 prints the JSON line.
+With N > 1 GPUs (torchrun, or ``--gpus N`` alone: bench.py then spawns one
+process per GPU itself) the same config-1 workload is split over the ranks
+by batch rows - strong scaling, no data-path collective (heads and rows are
+independent) - and times are the max over ranks.  Extras at N > 1: config 4
+head-sharded (strong, with per-rank K3 HBM fractions and the LPT balance),
+config 1 weak-scaled, and config 2 in gather mode (K3's combine stores every
+head's output into every rank's buffer over NVLink).  Rank 0 prints the
+JSON line.
 """
 
 from __future__ import annotations
@@ -191,95 +197,158 @@ def decode_bytes(w, res, lives):
     return out
 
 
+class Ranks:
+    """One process per GPU (RANK / WORLD_SIZE / LOCAL_RANK from torchrun or
+    from bench.py's own spawner).  NCCL carries only the barriers, the
+    max-over-ranks timings and small host objects: the hot path shards with
+    no data-path collective (heads / batch rows are independent,
+    engine.py:182-199, 236-259, 310-349)."""
+
+    def __init__(self):
+        import torch
+
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        # AKV_BENCH_ONE_DEVICE=1 (code-path check only): every rank on cuda:0
+        # over gloo, so the multi-rank path can be exercised on a one-GPU
+        # box; its numbers are not measurements
+        self.one_dev = os.environ.get("AKV_BENCH_ONE_DEVICE") == "1"
+        if self.one_dev:
+            self.local = 0
+        self.dist = None
+        if self.world > 1:
+            import torch.distributed as dist
+
+            torch.cuda.set_device(self.local)
+            if self.one_dev:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.dist = dist
+        self.dev = torch.device("cuda", self.local)
+        torch.cuda.set_device(self.dev)
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+
+    def max(self, *vals):
+        """Element-wise max over ranks of host floats."""
+        import torch
+
+        if self.dist is None:
+            return list(vals) if len(vals) > 1 else vals[0]
+        t = torch.tensor([float(v) for v in vals], dtype=torch.float64,
+                         device="cpu" if self.one_dev else self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        out = t.tolist()
+        return out if len(vals) > 1 else out[0]
+
+    def gather(self, obj):
+        """Host objects of every rank, in rank order."""
+        if self.dist is None:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+
+def _dec_inputs(qd, kd, vd, cd, N, D):
+    return ([qd[:, :, N + t] for t in range(D)], [kd[:, :, N + t] for t in range(D)],
+            [vd[:, :, N + t] for t in range(D)], [cd[:, N + t].contiguous() for t in range(D)])
+
+
+def _policy_counts(res):
+    fam = res.family
+    pol = np.bincount(res.choice[:, 0], minlength=len(fam))
+    return {str(fam[i]): int(pol[i]) for i in range(len(fam)) if pol[i]}
+
+
+def _merge_counts(parts):
+    out = {}
+    for d in parts:
+        for k, v in d.items():
+            out[k] = out.get(k, 0) + v
+    return out
+
+
 def bench_ours(args):
     import torch
 
+    from paper_2310_01801_b200.parallel import batch_shard
     from paper_2310_01801_b200.workloads import config1
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    dist = None
-    # AKV_BENCH_ONE_DEVICE=1 (code-path check only): every rank on cuda:0 over
-    # gloo, so the torchrun path can be exercised on a one-GPU box; its
-    # numbers are not measurements
-    one_dev = os.environ.get("AKV_BENCH_ONE_DEVICE") == "1"
-    if one_dev:
-        local = 0
-    if world > 1:
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        if one_dev:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
-    w = config1(seed=1 + rank)
+    R = Ranks()
+    rank, world, dev = R.rank, R.world, R.dev
+    full = config1(seed=1)
+    # strong scaling: the one config-1 workload, its batch rows split over the
+    # ranks (each rank's inputs are its slice of the same seeded streams)
+    sh = batch_shard(full.B, full.H, world, rank)
+    w = full.rows(sh.b0, sh.b1)
     T = args.T
     qd, kd, vd, cd, qh, kh, vh, clsh = make_inputs(w, dev)
     slopes = torch.tensor(w.slopes, dtype=torch.float32, device=dev)
     sinks = torch.tensor(w.sinks, dtype=torch.float32, device=dev)
     N, D = w.N, w.D
-    dec = ([qd[:, :, N + t] for t in range(D)], [kd[:, :, N + t] for t in range(D)],
-           [vd[:, :, N + t] for t in range(D)], [cd[:, N + t].contiguous() for t in range(D)])
+    dec = _dec_inputs(qd, kd, vd, cd, N, D)
 
     # untimed: live counts per step (for the algorithmic byte count)
     res, cache, lives = run_session(w, T, qd, kd, vd, cd, slopes, sinks, dec, record=True)
     cache.check()
     bytes_per_launch = decode_bytes(w, res, lives)
     kept0 = int(res.kept_count.sum())
-    pruned = 1.0 - float(lives[-1].sum()) / float(w.B * w.H * (N + D))
+    live_end = float(lives[-1].sum())
     del cache
 
     for _ in range(args.warmup):
         run_session(w, T, qd, kd, vd, cd, slopes, sinks, dec)
     torch.cuda.synchronize()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    if dist is not None:
-        dist.barrier()
+    R.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(R.local) as clk:
         t_wall = time.perf_counter()
         for s in range(args.steps):
             run_session(w, T, qd, kd, vd, cd, slopes, sinks, dec, ev=evs[s])
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall
-    if dist is not None:
-        dist.barrier()
+    R.barrier()
     enc_ms = [e[0].elapsed_time(e[1]) for e in evs]
     dec_ms = [e[1].elapsed_time(e[2]) for e in evs]
-    tot_ms = float(evs[0][0].elapsed_time(evs[-1][2]))
-    if dist is not None:
-        t = torch.tensor([tot_ms, max(enc_ms), max(dec_ms)], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms, enc_max, dec_max = t.tolist()
+    tot_ms_local = float(evs[0][0].elapsed_time(evs[-1][2]))
+    tot_ms = R.max(tot_ms_local)
     ms_per_step = tot_ms / args.steps
-    tokens = w.B * D * args.steps * world
+    tokens = full.B * D * args.steps                 # the whole job's decode tokens
     value = tokens / (tot_ms / 1e3)
     dec_avg_ms = statistics.mean(dec_ms)
     launch_us = dec_avg_ms * 1e3 / D
     avg_bytes = statistics.mean(bytes_per_launch)
     achieved = avg_bytes / (launch_us * 1e-6) / 1e9
     peaks, peak_kind = _peaks()
+    per_rank = R.gather({"rank": rank, "rows": [sh.b0, sh.b1], "heads": w.B * w.H,
+                         "session_ms": tot_ms_local / args.steps,
+                         "k3_us_per_step": launch_us, "k3_gbs": achieved,
+                         "k3_frac_of_hbm_peak": achieved / peaks.get("hbm_gbs"),
+                         "kept_after_profile": kept0, "live_end": live_end,
+                         "policies": _policy_counts(res)})
 
     # sweep over the config's other thresholds (1 warm + 1 timed session each)
     sweep = {}
-    for Ts in w.thresholds:
+    for Ts in full.thresholds:
         run_session(w, Ts, qd, kd, vd, cd, slopes, sinks, dec)
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        R.barrier()
         r2, c2, _ = run_session(w, Ts, qd, kd, vd, cd, slopes, sinks, dec, ev=e)
         torch.cuda.synchronize()
-        fam = r2.family
-        pol = np.bincount(r2.choice[:, 0], minlength=len(fam))
+        tot, enc, decm = R.max(e[0].elapsed_time(e[2]), e[0].elapsed_time(e[1]),
+                               e[1].elapsed_time(e[2]))
+        kept = sum(R.gather(c2.total_retained()))
         sweep[f"{Ts:g}"] = {
-            "tok_s": w.B * D / (e[0].elapsed_time(e[2]) / 1e3),
-            "profiling_ms": e[0].elapsed_time(e[1]),
-            "decode_ms": e[1].elapsed_time(e[2]),
-            "final_cache_tokens": c2.total_retained(),
-            "pruned_ratio": 1.0 - c2.total_retained() / float(w.B * w.H * (N + D)),
-            "policies": {str(fam[i]): int(pol[i]) for i in range(len(fam)) if pol[i]},
+            "tok_s": full.B * D / (tot / 1e3), "profiling_ms": enc, "decode_ms": decm,
+            "final_cache_tokens": kept,
+            "pruned_ratio": 1.0 - kept / float(full.B * full.H * (N + D)),
+            "policies": _merge_counts(R.gather(_policy_counts(r2))),
         }
 
     # K1 alone (both tcgen05 QK^T passes + the policy epilogue), CUDA events
@@ -298,10 +367,12 @@ def bench_ours(args):
     k1_flops = 2.0 * w.B * w.H * w.d * N * (N + 1)
     k1_tflops = k1_flops / (k1_avg * 1e-3) / 1e12
 
-    e2e = bench_e2e(w, T, args, qh, kh, vh, clsh, slopes, sinks, dev, dist)
+    e2e_ms = bench_e2e(w, T, args, qh, kh, vh, clsh, slopes, sinks, dev, R)
+    e2e = {"value": tokens / (R.max(e2e_ms["ms"]) / 1e3), "unit": "tok/s",
+           "h2d_bytes_per_step": sum(R.gather(e2e_ms["h2d"])),
+           "d2h_bytes_per_step": sum(R.gather(e2e_ms["d2h"])),
+           "overlap": e2e_ms["overlap"]}
 
-    if rank != 0:
-        return
     line = {
         "metric": "decode tok/s with adaptive KV at fixed T (session incl. profiling)",
         "value": value,
@@ -311,21 +382,24 @@ def bench_ours(args):
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (seeded N(0,1) Q/K/V, planted local/sink heads; see DESIGN.md)",
         "config": {
-            "workload": f"c1 Llama-7B-shape layer: B={w.B} H={w.H} d={w.d} N={N} D={D} bf16, T={T:g}",
-            "parallelism": f"dp{world} (independent batches per GPU)",
+            "workload": f"c1 Llama-7B-shape layer: B={full.B} H={full.H} d={full.d} N={N} D={D} "
+                        f"bf16, T={T:g}",
+            "parallelism": f"dp{world}: the batch rows split over the GPUs (strong scaling, "
+                           "no data-path collective)",
             "step": "one session: K1 profile + K2 compact + D K3 decode steps",
-            "l2": "inputs larger than L2: every decode step streams the ~130-200 MB arena (L2 126 MB)",
+            "l2": "inputs larger than L2: every decode step streams the ~130-200 MB arena (L2 126 MB)"
+                  if world == 1 else "per-GPU arena ~1/N of the config-1 arena",
         },
-        "profiling_ms_per_layer": statistics.mean(enc_ms),
-        "decode_only_tok_s": w.B * D / (dec_avg_ms / 1e3),
-        "decode_us_per_step": launch_us,
-        "kept_tokens_after_profile": kept0,
-        "pruned_ratio_end": pruned,
+        "profiling_ms_per_layer": R.max(statistics.mean(enc_ms)),
+        "decode_only_tok_s": full.B * D / (R.max(dec_avg_ms) / 1e3),
+        "decode_us_per_step": R.max(launch_us),
+        "kept_tokens_after_profile": sum(r["kept_after_profile"] for r in per_rank),
+        "pruned_ratio_end": 1.0 - sum(r["live_end"] for r in per_rank) / float(full.B * full.H * (N + D)),
         "sweep": sweep,
         "gpu_launches": args.steps * (5 + D),
         "roofline": {
@@ -337,9 +411,10 @@ def bench_ours(args):
             "unit": "GB/s",
             "frac": achieved / peaks.get("hbm_gbs"),
             "frac_of_spec_8tbs": achieved / 8000.0,   # report both denominators
-            "traffic": _traffic("k3_decode_mma<128, 2>"),
+            "traffic": _traffic("k3_decode_mma<128, 2>") if world == 1 else None,
             "algorithmic_bytes_per_launch": avg_bytes,
             "avg_launch_us": launch_us,
+            "scope": "rank 0" if world > 1 else "the GPU",
         },
         "profiling_roofline": {
             "kernel": "k1 (akv_profile: two tcgen05 QK^T passes, row lse + column sums, policy)",
@@ -362,63 +437,190 @@ def bench_ours(args):
         "wall_s": t_wall,
         "e2e": e2e,
     }
-    if world == 1 and not args.no_extras:
-        del qd, kd, vd, cd, dec
-        torch.cuda.empty_cache()
-        line["other_configs"] = bench_extras(T, dev, peaks)
+    if world > 1:
+        line["per_rank"] = per_rank
+    del qd, kd, vd, cd, dec
+    torch.cuda.empty_cache()
+    if not args.no_extras:
+        if world == 1:
+            line["other_configs"] = bench_extras(T, dev, peaks)
+        else:
+            line["other_configs"] = bench_extras_multi(T, R, peaks, args, rank0_line=line)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_port(w, T)
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def _c4_session(w, T, R, peaks):
+    """One warm + one timed config-4 session on this rank's shard; times are
+    the max over ranks."""
+    import torch
+
+    dev = R.dev
+    qd, kd, vd, cd, *_ = make_inputs(w, dev)
+    slopes = torch.tensor(w.slopes, dtype=torch.float32, device=dev)
+    sinks = torch.tensor(w.sinks, dtype=torch.float32, device=dev)
+    N, D = w.N, w.D
+    dec = _dec_inputs(qd, kd, vd, cd, N, D)
+    res, cache, lives = run_session(w, T, qd, kd, vd, cd, slopes, sinks, dec, record=True)
+    cache.check()
+    nbytes = statistics.mean(decode_bytes(w, res, lives))
+    costs = (res.kept_count.astype(np.int64) + D).tolist()
+    del cache
+    run_session(w, T, qd, kd, vd, cd, slopes, sinks, dec)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    R.barrier()
+    res, cache, _ = run_session(w, T, qd, kd, vd, cd, slopes, sinks, dec, ev=ev)
+    torch.cuda.synchronize()
+    enc, decm = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
+    gbs = nbytes / (decm * 1e-3 / D) / 1e9
+    out = {"enc_ms": enc, "dec_ms": decm, "gbs": gbs, "frac": gbs / peaks.get("hbm_gbs"),
+           "retained": cache.total_retained(), "policies": _policy_counts(res), "costs": costs}
+    del qd, kd, vd, cd, dec, cache
+    torch.cuda.empty_cache()
+    return out
 
 
 def bench_extras(T, dev, peaks):
     """Supplementary single-GPU measurements of BASELINE configs 4 and 2 (not
     the headline): one timed c4 session (long context, N=16384) and a c2
     decode (32-layer Llama-7B shape through the multi-layer caller)."""
-    import torch
-
-    from paper_2310_01801_b200 import ProfilerConfig
     from paper_2310_01801_b200.workloads import config4
+
+    class _One:
+        world, rank = 1, 0
+
+        def __init__(self, dev):
+            self.dev = dev
+
+        def barrier(self):
+            pass
 
     out = {}
     w = config4()
-    qd, kd, vd, cd, *_ = make_inputs(w, dev)
-    slopes = torch.tensor(w.slopes, dtype=torch.float32, device=dev)
-    sinks = torch.tensor(w.sinks, dtype=torch.float32, device=dev)
+    r = _c4_session(w, T, _One(dev), peaks)
     N, D = w.N, w.D
-    dec = ([qd[:, :, N + t] for t in range(D)], [kd[:, :, N + t] for t in range(D)],
-           [vd[:, :, N + t] for t in range(D)], [cd[:, N + t].contiguous() for t in range(D)])
-    res, cache, lives = run_session(w, T, qd, kd, vd, cd, slopes, sinks, dec, record=True)
-    cache.check()
-    nbytes = decode_bytes(w, res, lives)
-    del cache
-    run_session(w, T, qd, kd, vd, cd, slopes, sinks, dec)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    res, cache, _ = run_session(w, T, qd, kd, vd, cd, slopes, sinks, dec, ev=ev)
-    torch.cuda.synchronize()
-    enc, decm = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
-    fam = res.family
-    pol = np.bincount(res.choice[:, 0], minlength=len(fam))
-    gbs = statistics.mean(nbytes) / (decm * 1e-3 / D) / 1e9
     out["c4"] = {
         "workload": f"long context: B={w.B} H={w.H} d={w.d} N={N} D={D} bf16, T={T:g}",
-        "session_tok_s": w.B * D / ((enc + decm) * 1e-3), "profiling_ms": enc,
-        "k1_tflops_incl_policy_and_compaction": 2.0 * w.B * w.H * w.d * N * (N + 1) / (enc * 1e-3) / 1e12,
-        "decode_us_per_step": decm * 1e3 / D, "decode_achieved_gbs": gbs,
-        "decode_frac_of_hbm_peak": gbs / peaks.get("hbm_gbs"),
-        "pruned_ratio_end": 1.0 - cache.total_retained() / float(w.B * w.H * (N + D)),
-        "policies": {str(fam[i]): int(pol[i]) for i in range(len(fam)) if pol[i]},
+        "session_tok_s": w.B * D / ((r["enc_ms"] + r["dec_ms"]) * 1e-3),
+        "profiling_ms": r["enc_ms"],
+        "k1_tflops_incl_policy_and_compaction": 2.0 * w.B * w.H * w.d * N * (N + 1) / (r["enc_ms"] * 1e-3) / 1e12,
+        "decode_us_per_step": r["dec_ms"] * 1e3 / D, "decode_achieved_gbs": r["gbs"],
+        "decode_frac_of_hbm_peak": r["frac"],
+        "pruned_ratio_end": 1.0 - r["retained"] / float(w.B * w.H * (N + D)),
+        "policies": r["policies"],
     }
-    del qd, kd, vd, cd, dec, cache
+    out["c2"] = _c2_decode(T, dev, peaks)
+    return out
+
+
+def bench_extras_multi(T, R, peaks, args, rank0_line):
+    """N > 1: config 4 head-sharded over the ranks (strong scaling: 128 heads
+    -> 128/N per GPU) with per-rank K3 HBM fractions and the LPT balance of
+    the profiled decode costs; config 1 weak-scaled (an independent c1 batch
+    per rank); config 2 in gather mode (the Llama-7B stack head-sharded, K3's
+    combine storing every head's output into every rank's symmetric-memory
+    buffer over NVLink).  A watchdog prints the headline line and exits if
+    a multi-GPU extra does not finish (the peer-store path has only run on
+    one GPU before)."""
+    import threading
+
+    import torch
+
+    from paper_2310_01801_b200.parallel import (assignment_loads, head_shard, lpt_assignment)
+    from paper_2310_01801_b200.workloads import config1, config4
+
+    out = {}
+    limit = float(os.environ.get("AKV_BENCH_EXTRAS_TIMEOUT", "600"))
+
+    def _expire():
+        if R.rank == 0:
+            rank0_line["other_configs"] = dict(out, timeout=f"multi-GPU extras exceeded {limit:.0f} s")
+            print(json.dumps(rank0_line), flush=True)
+        os._exit(0)
+
+    dog = threading.Timer(limit, _expire)
+    dog.daemon = True
+    dog.start()
+
+    w4 = config4()
+    sh = head_shard(w4.B, w4.H, R.world, R.rank)
+    r = _c4_session(w4.heads(sh.h0, sh.h1), T, R, peaks)
+    enc, decm = R.max(r["enc_ms"], r["dec_ms"])
+    ranks = R.gather({k: r[k] for k in ("enc_ms", "dec_ms", "gbs", "frac", "retained", "costs")})
+    # decode cost per head (kept + D live rows), global (b, h) order
+    costs = np.zeros((w4.B, w4.H), np.int64)
+    for rr, part in enumerate(ranks):
+        s_ = head_shard(w4.B, w4.H, R.world, rr)
+        costs[:, s_.h0:s_.h1] = np.asarray(part["costs"]).reshape(w4.B, s_.h1 - s_.h0)
+    flat = costs.reshape(-1).tolist()
+    contig = [sum(part["costs"]) for part in ranks]
+    lpt = assignment_loads(flat, lpt_assignment(flat, R.world))
+    N, D = w4.N, w4.D
+    out["c4_head_sharded"] = {
+        "workload": f"long context: B={w4.B} H={w4.H} d={w4.d} N={N} D={D} bf16, T={T:g}; "
+                    f"{w4.H // R.world} heads x {w4.B} rows per GPU",
+        "scaling": "strong",
+        "session_tok_s": w4.B * D / ((enc + decm) * 1e-3), "profiling_ms": enc,
+        "decode_us_per_step": decm * 1e3 / D,
+        "per_rank": [{"rank": i, "decode_us_per_step": p["dec_ms"] * 1e3 / D,
+                      "k3_gbs": p["gbs"], "k3_frac_of_hbm_peak": p["frac"]}
+                     for i, p in enumerate(ranks)],
+        "balance": {"contiguous_max_over_mean": max(contig) / (sum(contig) / len(contig)),
+                    "lpt_max_over_mean": max(lpt) / (sum(lpt) / len(lpt)),
+                    "basis": "decode live rows per rank (kept + D per head) after profiling"},
+        "pruned_ratio_end": 1.0 - sum(p["retained"] for p in ranks) / float(w4.B * w4.H * (N + D)),
+    }
+
+    # weak scaling: an independent c1 batch per rank (seed offset by rank)
+    w1 = config1(seed=1 + R.rank)
+    qd, kd, vd, cd, *_ = make_inputs(w1, R.dev)
+    sl = torch.tensor(w1.slopes, dtype=torch.float32, device=R.dev)
+    sk = torch.tensor(w1.sinks, dtype=torch.float32, device=R.dev)
+    dec = _dec_inputs(qd, kd, vd, cd, w1.N, w1.D)
+    for _ in range(2):
+        run_session(w1, T, qd, kd, vd, cd, sl, sk, dec)
+    steps = 3
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    R.barrier()
+    torch.cuda.synchronize()
+    ev[0].record()
+    for _ in range(steps):
+        run_session(w1, T, qd, kd, vd, cd, sl, sk, dec)
+    ev[1].record()
+    torch.cuda.synchronize()
+    ms = R.max(ev[0].elapsed_time(ev[1]))
+    out["c1_weak"] = {"workload": "an independent c1 batch per GPU (B=8 each)", "scaling": "weak",
+                      "tok_s": R.world * w1.B * w1.D * steps / (ms / 1e3),
+                      "ms_per_session": ms / steps}
+    del qd, kd, vd, cd, dec
     torch.cuda.empty_cache()
 
-    from paper_2310_01801_b200.llama import LLAMA_7B, FastGenLlama
+    if not R.one_dev:   # ranks sharing one GPU would spin on each other's barriers
+        try:
+            out["c2_gather"] = _c2_decode(T, R.dev, peaks, R=R)
+        except Exception as e:  # noqa: BLE001  (reported, never a silent fallback)
+            out["c2_gather"] = {"error": f"{type(e).__name__}: {e}"[:300]}
+    dog.cancel()
+    return out
 
-    B, N, D = 16, 2048, 512
-    model = FastGenLlama(LLAMA_7B, seed=0, max_positions=N + D + 8)
-    rng = np.random.default_rng([0, 2])
+
+def _c2_decode(T, dev, peaks, R=None):
+    """Config 2 decode through the multi-layer caller: on one GPU the whole
+    Llama-7B stack; with ranks, gather mode (heads sharded, the attention
+    outputs stored by K3's combine into every rank's buffer)."""
+    import torch
+
+    from paper_2310_01801_b200 import ProfilerConfig
+    from paper_2310_01801_b200.llama import LLAMA_7B, FastGenLlama, ShardPlan
     from paper_2310_01801_b200.workloads import PUNCT_IDS, PUNCT_PROB, SPECIAL_IDS
 
+    world = 1 if R is None else R.world
+    plan = ShardPlan() if world == 1 else ShardPlan(R.rank, world, "gather")
+    B, N, D = 16, 2048, 512
+    model = FastGenLlama(LLAMA_7B, seed=0, max_positions=N + D + 8, plan=plan)
+    rng = np.random.default_rng([0, 2])
     ids = rng.integers(0, LLAMA_7B.vocab, size=(B, N))
     punct = rng.random((B, N)) < PUNCT_PROB
     ids = np.where(punct, np.asarray(PUNCT_IDS)[rng.integers(0, len(PUNCT_IDS), (B, N))], ids)
@@ -430,6 +632,9 @@ def bench_extras(T, dev, peaks):
         model.decode_step()
     model.caches = []
     e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    if R is not None:
+        R.barrier()
+    torch.cuda.synchronize()
     e[0].record()
     pre = model.prefill(tokens, pc, max_new_tokens=D)
     e[1].record()
@@ -441,22 +646,29 @@ def bench_extras(T, dev, peaks):
     torch.cuda.synchronize()
     model.check()
     pre_ms, dec_ms = e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2])
-    cfg = LLAMA_7B
-    wbytes = 2 * (cfg.n_layers * (4 * cfg.d_model * cfg.d_model + 3 * cfg.d_model * cfg.ffn)
-                  + cfg.vocab * cfg.d_model)
-    kv = 2 * cfg.n_layers * B * cfg.n_heads * cfg.head_dim * 2 * (N + D / 2)  # mean live rows
     replay_ms = e[3].elapsed_time(e[2]) / (D - 1)
+    if R is not None:
+        pre_ms, dec_ms, replay_ms = R.max(pre_ms, dec_ms, replay_ms)
+    cfg = LLAMA_7B
+    # per-GPU bytes of a step: in gather mode a rank streams its heads' KV and
+    # QKV rows, and the replicated O / MLP / lm_head weights
+    dm, F, Hl = cfg.d_model, cfg.ffn, model.Hl
+    wbytes = 2 * (cfg.n_layers * (3 * Hl * cfg.head_dim * dm + dm * dm + 3 * dm * F)
+                  + cfg.vocab * dm)
+    kv = 2 * cfg.n_layers * B * Hl * cfg.head_dim * 2 * (N + D / 2)  # mean live rows
     step_s = replay_ms * 1e-3   # graph replays; the eager first step + capture is reported apart
-    out["c2"] = {
+    out = {
         "workload": f"Llama-7B shape, 32 layers, random bf16 weights, B={B} prompt {N} greedy "
-                    f"decode {D}, T={T:g}",
+                    f"decode {D}, T={T:g}" + ("" if world == 1 else
+                                               f"; gather mode, {Hl} heads per GPU"),
         "decode_tok_s": B * D / (dec_ms * 1e-3), "decode_ms_per_step": dec_ms / D,
         "first_step_ms": e[1].elapsed_time(e[3]),
         "replay_ms_per_step": replay_ms, "replay_tok_s": B / step_s,
         "prefill_ms": pre_ms, "profiling_ms_per_layer": float(np.mean(pre.profiling_ms())),
-        "step_hbm_bytes": wbytes + kv, "step_roofline_basis": "replay steps", "step_achieved_gbs": (wbytes + kv) / step_s / 1e9,
+        "step_hbm_bytes_per_gpu": wbytes + kv, "step_roofline_basis": "replay steps",
+        "step_achieved_gbs_per_gpu": (wbytes + kv) / step_s / 1e9,
         "step_frac_of_hbm_peak": (wbytes + kv) / step_s / 1e9 / peaks.get("hbm_gbs"),
-        "cache_tokens_end": model.cache_tokens(),
+        "cache_tokens_end": model.cache_tokens() if R is None else sum(R.gather(model.cache_tokens())),
     }
     del model
     torch.cuda.empty_cache()
@@ -476,7 +688,7 @@ def _exp_roofline(w, k1_ms, clk):
             "exps_per_launch": exps}
 
 
-def bench_e2e(w, T, args, qh, kh, vh, clsh, slopes, sinks, dev, dist):
+def bench_e2e(w, T, args, qh, kh, vh, clsh, slopes, sinks, dev, R):
     """Same sessions through the public API from pinned HOST buffers: the
     H2D copies of every session's prompt and of every decode token's q/k/v
     rows and class, and the D2H copies of every step's output, are inside
@@ -574,8 +786,7 @@ def bench_e2e(w, T, args, qh, kh, vh, clsh, slopes, sinks, dev, dist):
         session(prefetch_next=True)
     main.wait_stream(cs)
     torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
+    R.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     state["slot"] = 0
     e0.record(main)          # the timed region starts with the first upload
@@ -587,16 +798,9 @@ def bench_e2e(w, T, args, qh, kh, vh, clsh, slopes, sinks, dev, dist):
     e1.record(main)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    world = 1
-    if dist is not None:
-        world = dist.get_world_size()
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     h2d = 3 * B * H * N * d * es + B * N + D * row_bytes
     d2h = D * B * H * d * 4
-    return {"value": world * B * D * args.steps / (ms / 1e3), "unit": "tok/s",
-            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+    return {"ms": ms, "h2d": int(h2d), "d2h": int(d2h),
             "overlap": "copy stream; prompt + packed token rows per session double-buffered, "
                        "outputs in 128-step chunks"}
 
@@ -817,6 +1021,22 @@ def bench_reference(args):
     }), flush=True)
 
 
+def _spawned_rank(index, world, port, argv):
+    os.environ.update({"RANK": str(index), "LOCAL_RANK": str(index), "WORLD_SIZE": str(world),
+                       "LOCAL_WORLD_SIZE": str(world), "MASTER_ADDR": "127.0.0.1",
+                       "MASTER_PORT": str(port)})
+    sys.argv = argv
+    main()
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        return s_.getsockname()[1]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -833,8 +1053,19 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         bench_reference(args)
-    else:
-        bench_ours(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # not under torchrun: one process per GPU, spawned here
+        import torch.multiprocessing as tmp
+
+        tmp.spawn(_spawned_rank, args=(args.gpus, _free_port(), list(sys.argv)),
+                  nprocs=args.gpus, join=True)
+        return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; using {world} ranks",
+              file=sys.stderr)
+    bench_ours(args)
 
 
 if __name__ == "__main__":

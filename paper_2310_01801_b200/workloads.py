@@ -23,7 +23,7 @@ subset of heads at full size).
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 
@@ -75,6 +75,23 @@ class Workload:
     seed: int = 0
     slopes: np.ndarray = field(default=None)
     sinks: np.ndarray = field(default=None)
+    row0: int = 0     # global index of local batch row 0 (a rank's shard)
+    head0: int = 0    # global index of local head 0
+
+    def rows(self, b0: int, b1: int) -> "Workload":
+        """Batch rows [b0, b1) of this workload as a workload of their own
+        (same seeded streams: a shard's inputs equal its slice of the whole)."""
+        if not 0 <= b0 < b1 <= self.B:
+            raise ValueError(f"rows [{b0}, {b1}) outside B={self.B}")
+        return replace(self, B=b1 - b0, row0=self.row0 + b0)
+
+    def heads(self, h0: int, h1: int) -> "Workload":
+        """Heads [h0, h1) of every batch row (head sharding)."""
+        if not 0 <= h0 < h1 <= self.H:
+            raise ValueError(f"heads [{h0}, {h1}) outside H={self.H}")
+        return replace(self, H=h1 - h0, head0=self.head0 + h0,
+                       slopes=np.asarray(self.slopes)[h0:h1].copy(),
+                       sinks=np.asarray(self.sinks)[h0:h1].copy())
 
     @property
     def total_len(self) -> int:
@@ -89,7 +106,7 @@ class Workload:
 
     def tokens(self, b: int) -> np.ndarray:
         """Token ids [N+D] of batch row b."""
-        rng = np.random.default_rng([self.seed, b, 1_000_003])
+        rng = np.random.default_rng([self.seed, b + self.row0, 1_000_003])
         n = self.total_len
         ids = rng.integers(0, VOCAB_SIZE, size=n)
         punct = rng.random(n) < PUNCT_PROB
@@ -103,7 +120,7 @@ class Workload:
 
     def head_qkv(self, b: int, h: int) -> tuple:
         """(q, k, v) float32 [N+D, d] of one head, dtype-rounded."""
-        rng = np.random.default_rng([self.seed, b, h])
+        rng = np.random.default_rng([self.seed, b + self.row0, h + self.head0])
         x = rng.standard_normal((3, self.total_len, self.d), dtype=np.float32)
         if self.dtype == "bf16":
             x = round_bf16(x)

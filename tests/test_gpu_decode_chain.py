@@ -23,10 +23,15 @@ pytestmark = pytest.mark.gpu
 
 
 def _workload(B, H, N, D, d, seed):
-    rng = np.random.default_rng([seed, 99])
-    sinks = np.where(rng.random(H) < 0.6, rng.uniform(7.0, 11.0, H), 0.0)
-    slopes = np.where(rng.random(H) < 0.3, 0.05, 0.0)
-    return Workload("chain", B, H, N, D, d, "bf16", (0.99,), seed=seed, slopes=slopes,
+    """Sink strengths graded so that at T=0.98 the heads mix `special`,
+    `special+punct+frequent` (evicting every step) and `full`."""
+    if H <= 12:
+        sinks = np.array([11.0, 0.0, 9.5, 10.5, 0.0, 12.0, 8.5, 11.0, 0, 10, 9, 0])[:H]
+        slopes = np.array([0, 0.05, 0.05, 0, 0, 0, 0.05, 0, 0, 0, 0.05, 0])[:H]
+    else:
+        sinks = np.tile([11.0, 0.0, 9.5, 10.5], H // 4)
+        slopes = np.tile([0, 0.05, 0, 0.05], H // 4)
+    return Workload("chain", B, H, N, D, d, "bf16", (0.98,), seed=seed, slopes=slopes,
                     sinks=sinks)
 
 
@@ -66,8 +71,8 @@ def _session(w, T, chained, rows=None, kept_every=1):
 @pytest.mark.parametrize("d,H", [(128, 4), (128, 12), (64, 6)])
 def test_chained_steps_bit_identical(d, H):
     w = _workload(1, H, 700, 96, d, seed=5 + d + H)
-    r0, o0, k0 = _session(w, 0.99, chained=False)
-    r1, o1, k1 = _session(w, 0.99, chained=True)
+    r0, o0, k0 = _session(w, 0.98, chained=False)
+    r1, o1, k1 = _session(w, 0.98, chained=True)
     np.testing.assert_array_equal(r0.choice, r1.choice)
     assert not all(r0.family[c].is_full for c in r0.choice[:, 0]), "every head full: no eviction"
     np.testing.assert_array_equal(o0, o1)
@@ -79,9 +84,9 @@ def test_chained_steps_bit_identical(d, H):
 def test_more_than_2048_heads_per_call():
     """B=72 x H=32 = 2,304 heads: two launches per step (64 + 8 rows)."""
     w = _workload(72, 32, 160, 24, 128, seed=11)
-    r, o, k = _session(w, 0.99, chained=True, kept_every=8)
-    ra, oa, ka = _session(w, 0.99, chained=True, rows=list(range(64)), kept_every=8)
-    rb, ob, kb = _session(w, 0.99, chained=True, rows=list(range(64, 72)), kept_every=8)
+    r, o, k = _session(w, 0.98, chained=True, kept_every=8)
+    ra, oa, ka = _session(w, 0.98, chained=True, rows=list(range(64)), kept_every=8)
+    rb, ob, kb = _session(w, 0.98, chained=True, rows=list(range(64, 72)), kept_every=8)
     G1 = 64 * w.H
     np.testing.assert_array_equal(r.choice[:G1], ra.choice)
     np.testing.assert_array_equal(r.choice[G1:], rb.choice)
@@ -99,9 +104,9 @@ def test_more_than_2048_heads_per_call():
         cls = lut[w.tokens(b)].astype(np.int64)
         q, kk, v = (x.astype(np.float64) for x in w.head_qkv(b, h))
         N = w.N
-        prof = O.profile_head(q[:N], kk[:N], v[:N], cls, w.slopes[h], w.sinks[h], fam, [0.99])
+        prof = O.profile_head(q[:N], kk[:N], v[:N], cls, w.slopes[h], w.sinks[h], fam, [0.98])
         assert int(r.choice[g, 0]) == int(prof.choice[0]) or \
-            np.any(np.abs(prof.recoveries[:max(int(prof.choice[0]), int(r.choice[g, 0])) + 1] - 0.99) < 1e-4)
+            np.any(np.abs(prof.recoveries[:max(int(prof.choice[0]), int(r.choice[g, 0])) + 1] - 0.98) < 1e-4)
         if int(r.choice[g, 0]) != int(prof.choice[0]):
             continue
         st = O.compact_head(prof, kk[:N], v[:N], fam[prof.choice[0]], N, w.slopes[h], w.sinks[h])
