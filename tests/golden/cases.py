@@ -83,6 +83,11 @@ CASES = {
     "c0_fixed_spfl": (_c0_sink, dict(fixed="special+punct+frequent(r_f=0.3)+local(r_l=0.3)")),
     "c0_fixed_freq": (_c0_sink, dict(fixed="frequent(r_f=0.25)")),
     "c1_small": (_c1_small, dict(decode_T=0.98)),
+    # the tcgen05 profiling path's secondary outputs (bf16, d=128): the
+    # cosine criterion (colsq, profiler.py:148-178) and last-row recovery
+    # (profiler.py:84-85)
+    "c1_small_cosine": (_c1_small, dict(decode_T=0.98, criterion="cosine")),
+    "c1_small_last": (_c1_small, dict(decode_T=0.98, rows="last")),
     "c1_heads": (_c1_heads, dict(decode_T=0.98, heads="planted+2")),
     "c4_heads": (_c4_heads, dict(decode_T=0.95, heads=[(1, 0), (1, 3), (1, 18)])),
 }

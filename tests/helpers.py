@@ -57,7 +57,7 @@ def oracle_case(name):
     fixed = parse_fixed(opts["fixed"]) if "fixed" in opts else None
     fam = [fixed] if fixed else case_family(w, opts)
     N, D = w.N, w.D
-    res = dict(R=[], cost=[], choice=[], colsum=[], lastrow=[], enc_kept=[], enc_out=[],
+    res = dict(R=[], cost=[], cos=[], choice=[], colsum=[], lastrow=[], enc_kept=[], enc_out=[],
                dec_kept=np.zeros((D, len(heads), N + D), bool),
                dec_out=np.zeros((D, len(heads), w.d)), dec_choice=[],
                dec_rec=np.zeros((D + 1, len(heads))))
@@ -69,6 +69,7 @@ def oracle_case(name):
                               hd["sink"], fam, thr + ([dec_T] if not fixed else []), rows, crit)
         res["R"].append(prof.recoveries)
         res["cost"].append(prof.costs)
+        res["cos"].append(prof.cosine)
         res["choice"].append(prof.choice[:len(thr)])
         res["colsum"].append(prof.colsum)
         res["lastrow"].append(prof.lastp)
@@ -90,7 +91,7 @@ def oracle_case(name):
             res["dec_kept"][t, gi, st.positions] = True
             res["dec_out"][t, gi] = o
             res["dec_rec"][t + 1, gi] = st.recovery
-    for k in ("R", "cost", "choice", "colsum", "lastrow", "enc_kept", "enc_out", "dec_choice"):
+    for k in ("R", "cost", "cos", "choice", "colsum", "lastrow", "enc_kept", "enc_out", "dec_choice"):
         res[k] = np.asarray(res[k])
     return res
 

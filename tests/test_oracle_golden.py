@@ -17,6 +17,8 @@ def test_oracle_matches_reference_golden(name):
     # profiling: every family member's recovery and cost, the choice per T
     np.testing.assert_allclose(o["R"], g["R"], rtol=0, atol=1e-12)
     np.testing.assert_array_equal(o["cost"], g["cost"])
+    # masked cosine similarity of every member (profiler.py:148-161)
+    np.testing.assert_allclose(o["cos"], g["cos"], rtol=0, atol=1e-12)
     if g["choice"].size and "fixed" not in C.CASES[name][1]:
         np.testing.assert_array_equal(o["choice"], g["choice"])
     np.testing.assert_array_equal(o["dec_choice"], g["dec_choice"])
