@@ -348,8 +348,38 @@ def make_trace():
                                            for k in grid}) for r in res.records]))
 
 
+NUCLEUS = ((0.8, 0.9, 3), (1.5, 0.5, 11), (0.3, 1.0, 0))
+
+
+def make_nucleus():
+    """The reference's nucleus sampler (engine.py:71-90): (1) tokens drawn by
+    its _Sampler from seeded logit vectors; (2) generate() with Nucleus on
+    the recorded replay trace (replay.akvt, written by make_trace)."""
+    from adaptive_kv.engine import GenerationConfig, Nucleus, _Sampler, generate
+    from adaptive_kv.trace import TraceModel, read_trace
+
+    rng = np.random.default_rng(2024)
+    logits = rng.standard_normal((64, 40)) * 3.0
+    draws = []
+    for temp, top_p, seed in NUCLEUS:
+        smp = _Sampler(Nucleus(temperature=temp, top_p=top_p, seed=seed))
+        draws.append([smp(row) for row in logits])
+    z = dict(np.load(C.golden_path("replay")))
+    P, S = int(z["prompt_len"]), int(z["steps"])
+    model = TraceModel(read_trace(os.path.join(C.HERE, "replay.akvt")))
+    prompt = model.prompt_token_ids(P)
+    gen = []
+    for temp, top_p, seed in NUCLEUS:
+        res = generate(model, prompt, ProfilerConfig(recovery_threshold=0.95),
+                       GenerationConfig(max_new_tokens=S,
+                                        sampling=Nucleus(temperature=temp, top_p=top_p, seed=seed)))
+        gen.append(res.tokens)
+    np.savez_compressed(C.golden_path("nucleus"), params=np.array(NUCLEUS), logits=logits,
+                        draws=np.array(draws), gen_tokens=np.array(gen))
+
+
 def main(argv):
-    names = argv or list(C.CASES) + [C.MIXED["name"], "metrics", "replay"]
+    names = argv or list(C.CASES) + [C.MIXED["name"], "metrics", "replay", "nucleus"]
     for name in names:
         t0 = time.time()
         if name == C.MIXED["name"]:
@@ -358,6 +388,8 @@ def main(argv):
             make_metrics()
         elif name == "replay":
             make_trace()
+        elif name == "nucleus":
+            make_nucleus()
         else:
             make_workload_case(name)
         print(f"{name}: {time.time() - t0:.1f}s", flush=True)

@@ -100,12 +100,14 @@ def test_headline_session_every_head_every_step(T):
     res, enc, kept, outs = _gpu_session(w, T)
     ref = _oracle(w, T)
     G, D = w.B * w.H, w.D
-    near_t, mismatches = [], []
+    near_t, near_t_agree, mismatches = [], [], []
     for g, r in enumerate(ref):
         cg, co = int(res.choice[g, 0]), r["choice"]
         upto = max(cg, co) + 1
         if np.any(np.abs(r["R"][:upto] - T) < NEAR_T) or np.any(np.abs(res.recovery[g, :upto] - T) < NEAR_T):
             near_t.append(g)
+            if cg == co and np.array_equal(enc[g], r["enc"]) and np.array_equal(kept[:, g], r["kept"]):
+                near_t_agree.append(g)
             continue
         if cg != co:
             mismatches.append((g, "policy", cg, co))
@@ -130,5 +132,5 @@ def test_headline_session_every_head_every_step(T):
     evicting = int(sum(1 for g in keep if not fam[res.choice[g, 0]].is_full))
     print(f"headline T={T}: {len(keep)} of {G} heads compared over {D} steps "
           f"({len(keep) * D} head-steps, {evicting} evicting heads), 0 policy / kept-set "
-          f"mismatches; near-T heads listed separately: {near_t}; max |o - o_ref| / max|o_ref| "
+          f"mismatches; near-T heads listed separately: {near_t} (of which policy and every kept set agree anyway: {near_t_agree}); max |o - o_ref| / max|o_ref| "
           f"= {worst:.2e}; policies {dict((str(fam[i]), int(pol[i])) for i in range(len(fam)) if pol[i])}")

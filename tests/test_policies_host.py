@@ -120,3 +120,24 @@ def test_classification_special_wins_and_warns():
     assert [a.klass for a in anns] == [TokenClass.SPECIAL, TokenClass.SPECIAL,
                                        TokenClass.PUNCTUATION, TokenClass.OTHER]
     assert vocab.class_codes([1, 2, 3, 4]).tolist() == [1, 1, 2, 0]
+
+
+def test_nucleus_sampler_matches_reference_draws():
+    """engine.py:71-90: the restated nucleus sampler draws the same tokens
+    as the reference's _Sampler on seeded logits (golden from the reference,
+    tests/golden/make_golden.py nucleus)."""
+    import numpy as np
+
+    import cases as C
+    from paper_2310_01801_b200.engine import EngineError, Nucleus, _Sampler
+
+    z = dict(np.load(C.golden_path("nucleus")))
+    for (temp, top_p, seed), want in zip(z["params"], z["draws"]):
+        smp = _Sampler(Nucleus(temperature=float(temp), top_p=float(top_p), seed=int(seed)))
+        assert [smp(row) for row in z["logits"]] == want.tolist()
+    import pytest
+
+    with pytest.raises(EngineError, match="temperature"):
+        Nucleus(temperature=0.0)
+    with pytest.raises(EngineError, match="top_p"):
+        Nucleus(top_p=1.5)

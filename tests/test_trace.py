@@ -189,3 +189,22 @@ def test_replay_through_gpu_matches_reference():
     assert [str(p) for p in choice] == [r[2] for r in ref[1:]]
     last = res.records[len(trace.tokens) - P]
     np.testing.assert_array_equal(cache.head_retained(), [last.head_retained[k] for k in grid])
+
+
+@pytest.mark.gpu
+def test_generate_with_nucleus_sampling_matches_reference():
+    """generate() with the reference's Nucleus sampler (engine.py:71-90,
+    382-394) on the recorded trace: the same sampled tokens as the
+    reference's own run (tests/golden/nucleus.npz)."""
+    from paper_2310_01801_b200 import GenerationConfig, Nucleus, ProfilerConfig, generate, read_trace
+
+    z = dict(np.load(C.golden_path("replay")))
+    n = dict(np.load(C.golden_path("nucleus")))
+    P, S = int(z["prompt_len"]), int(z["steps"])
+    model = TraceModel(read_trace(REPLAY_AKVT))
+    prompt = model.prompt_token_ids(P)
+    for (temp, top_p, seed), want in zip(n["params"], n["gen_tokens"]):
+        res = generate(model, prompt, ProfilerConfig(recovery_threshold=0.95),
+                       GenerationConfig(max_new_tokens=S, sampling=Nucleus(
+                           temperature=float(temp), top_p=float(top_p), seed=int(seed))))
+        assert res.tokens == want.tolist(), (temp, top_p, seed)
