@@ -169,6 +169,22 @@ def config1(seed: int = 1, B: int = 8, H: int = 32, N: int = 1024, D: int = 512)
                     slopes=slopes, sinks=sinks)
 
 
+def config1_frequent(seed: int = 1, B: int = 8, H: int = 32, N: int = 1024,
+                     D: int = 512) -> Workload:
+    """Config-1 shapes in the paper's compression regime (PAPER.md:473-475,
+    ~40 % pruned): a sink on EVERY head, strengths seeded uniform in
+    [9.6, 11.0] logits, no local bias.  At T=0.98 about three quarters of the
+    heads profile special+punct+frequent(+local) and evict at every decode
+    step (the FREQUENT score update and top-k run on most heads), the rest
+    special+punct or full.  Not a BASELINE config: the workload of the K3
+    FREQUENT-heavy measurement."""
+    rng = np.random.default_rng([seed, 31337])
+    sinks = rng.uniform(9.6, 11.0, H)
+    w = Workload("c1_frequent", B, H, N, D, 128, "bf16", (0.98,), seed=seed,
+                 slopes=np.zeros(H), sinks=sinks)
+    return w
+
+
 def config4(seed: int = 4, B: int = 4, H: int = 32, N: int = 16384, D: int = 256) -> Workload:
     """BASELINE config 4 (long-context stress): B=4, H=32, N=16384, D=256."""
     slopes, sinks = _planted(H, seed)
@@ -176,4 +192,4 @@ def config4(seed: int = 4, B: int = 4, H: int = 32, N: int = 16384, D: int = 256
                     slopes=slopes, sinks=sinks)
 
 
-CONFIGS = {"c0": config0, "c1": config1, "c4": config4}
+CONFIGS = {"c0": config0, "c1": config1, "c4": config4, "c1_frequent": config1_frequent}
