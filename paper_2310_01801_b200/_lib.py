@@ -11,7 +11,9 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libakv_sm100a.so")
+# AKV_LIB (experiments only): load another build of the library, e.g. an
+# A/B variant built by tools/build_variant.sh
+LIB_PATH = os.environ.get("AKV_LIB") or os.path.join(_HERE, "libakv_sm100a.so")
 
 AKV_OK, AKV_ERR_INVALID, AKV_ERR_CAPACITY, AKV_ERR_UNSUPPORTED, AKV_ERR_CUDA = range(5)
 DTYPE_F32, DTYPE_BF16 = 0, 1

@@ -56,7 +56,6 @@ namespace akv {
 constexpr int kStages = 3;  // SIMT (fp32 / small d) variant; the tcgen05-era mma kernel takes ST
 constexpr int kPageBytes = 16384;  // per K (and per V) page
 constexpr int kMaxHeads = 2048;
-constexpr int kMaxGrid = 320;   // decode CTAs per launch (2 per SM on a 148-SM B200)
 constexpr int kEpr = 8;   // candidates per thread per batch in the epilogue passes
 constexpr int kSmemEvict = 64;  // evictions per head-step paired through shared memory
 
@@ -99,7 +98,6 @@ struct DecParams {
   int peer_bf16;
   int l2_prefetch;            // pages prefetched into L2 ahead of the shared-memory ring
   int consumer_tail;          // consumers publish the CTA's last full-cache segment
-  int pre_pages;              // filler pages a CTA streams before its whole heads (mixed plan)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -120,8 +118,6 @@ __device__ __forceinline__ int page_owner(long long pg, long long P, int grid) {
 
 struct HeadCtx {
   int g, L, n;
-  int k;    // index of the head in the launch's page order (== g for the even plan)
-  int seg;  // mixed plan: which of the CTA's ranges the segment lies in (0 pre, 1 whole, 2 post)
   int pos;  // position of the inserted token
   int64_t base;
   uint8_t atoms;
@@ -132,8 +128,6 @@ struct HeadCtx {
 
 __device__ __forceinline__ void load_head(const DecParams& p, int g, int L, HeadCtx& hc) {
   hc.g = g;
-  hc.k = g;
-  hc.seg = 0;
   hc.L = L;
   hc.n = L + 1;
   hc.base = p.seg_off[g];
@@ -186,152 +180,37 @@ __device__ __forceinline__ long long plan_pages(const DecParams& p, int page, in
   return s_prefix[G];
 }
 
-// Page plan of the TMA/mma kernel ("mixed" plan), computed by every CTA
-// from live-count BOUNDS (base_live + step): exact for full-cache heads,
-// whose live count grows by one per step, an upper bound otherwise
-// (surplus pages stream as empty), so it is computable before the previous
-// step has finished.
-//
-// Evicting heads that fit in one CTA's share of the pages ("whole" heads)
-// are never split: each is streamed by one CTA, at the START of that CTA's
-// work, and combined straight from shared memory - no split-K partial, no
-// semaphore - while its epilogue (score update, top-k, eviction) runs on the
-// epilogue warps in parallel with the CTA streaming the rest of its share.
-// The remaining heads (full-cache heads and evicting heads larger than a
-// share) fill every CTA up to an equal share, split across CTAs (split-K).
-//
-// Page order: whole heads first (order index k < nW), then the others.
-// CTA c streams, in this order: "pre" filler pages [R[2c], R[2c+1]) (full
-// heads: they stream before the previous step has drained), its whole heads
-// [W[c], W[c+1]), then "post" filler pages [R[2c+1], R[2c+2]) (streamed
-// while the epilogue warps run the whole heads' policies).  The filler
-// ranges, in the order pre_0, post_0, pre_1, ..., tile the non-whole pages;
-// a head split across several of them is combined split-K, its part index
-// counting the non-empty ranges before (Rn).
-struct MixedPlan {
-  const int* prefix;  // [G+1] page prefix in page order
-  const int* R;       // [2*grid+1] filler range starts (flattened page index)
-  const int* Rn;      // [2*grid+1] non-empty filler ranges before range r
-  int nW, grid;
-  // filler range holding page pg (largest r with R[r] <= pg)
-  __device__ __forceinline__ int owner(long long pg) const {
-    int lo = 0, hi = 2 * grid - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (R[mid] <= pg) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-  }
-  // seg: 0 = this CTA's pre range, 1 = its whole heads, 2 = its post range
-  __device__ __forceinline__ void parts(int k, int seg, int* nparts, int* idx) const {
-    if (k < nW) { *nparts = 1; *idx = 0; return; }
-    const int o0 = owner(prefix[k]), o1 = owner(prefix[k + 1] - 1);
-    *nparts = Rn[o1] - Rn[o0] + 1;
-    *idx = Rn[2 * blockIdx.x + (seg == 2)] - Rn[o0];
-  }
-};
-
-struct PlanSmem {
-  int* prefix;    // [G+1]
-  int* order;     // [G] head at page-order index k
-  int* live;      // [G] live bound by head
-  uint8_t* full;  // [G]
-  int* W;         // [grid+1]
-  int* R;         // [2*grid+1]
-  int* Rn;        // [2*grid+1]
-};
-
-// Returns the total page count; *grid_out = CTAs with work, *nW_out = whole heads.
-__device__ long long plan_mixed(const DecParams& p, int page, int step, const PlanSmem& sm,
-                                int* red_i, int* grid_out, int* nW_out) {
-  const int G = p.G, T = blockDim.x, tid = threadIdx.x;
-  const int per = (G + T - 1) / T;
-  const int lo = min(G, tid * per), hi = min(G, lo + per);
+// Page plan from live-count BOUNDS (base_live + step), computable before
+// the previous step has finished: exact for full-cache heads (their live
+// count grows by one per step), an upper bound otherwise (surplus pages are
+// streamed as empty).  s_full marks full-cache heads.
+__device__ __forceinline__ long long plan_pages_bound(const DecParams& p, int page, int step,
+                                                      int* s_prefix, int* s_live,
+                                                      uint8_t* s_full, int* red_i) {
+  const int G = p.G;
+  const int per = (G + blockDim.x - 1) / blockDim.x;
+  const int lo = min(G, (int)threadIdx.x * per), hi = min(G, lo + per);
   int cnt = 0;
   for (int g = lo; g < hi; ++g) {
     const int want = p.base_live[g] + step;
-    const bool full = (p.atoms[g] & AKV_ATOM_FULL) != 0;
     // a full-cache head's live count is exactly base_live + step: past its
     // segment the insert cannot fit (flag it; writes stay in bounds)
-    if (want > p.seg_cap[g] - 1 && full && blockIdx.x == 0) atomicExch(p.status, AKV_ERR_CAPACITY);
+    if (want > p.seg_cap[g] - 1 && (p.atoms[g] & AKV_ATOM_FULL) && blockIdx.x == 0)
+      atomicExch(p.status, AKV_ERR_CAPACITY);
     const int bound = min(want, p.seg_cap[g] - 1);
-    sm.live[g] = bound;
-    sm.full[g] = full ? 1 : 0;
+    s_live[g] = bound;
+    s_full[g] = (p.atoms[g] & AKV_ATOM_FULL) ? 1 : 0;
     cnt += (bound + 1 + page - 1) / page;
   }
-  int P;
-  block_exclusive_scan<BlockSync>(cnt, red_i, &P);
-  const int grid = P < (int)gridDim.x ? P : (int)gridDim.x;
-  const int S = (P + grid - 1) / grid;  // pages per CTA share
-  int wc = 0, wp = 0, oc = 0, op = 0;
+  int total;
+  int off = block_exclusive_scan<BlockSync>(cnt, red_i, &total);
   for (int g = lo; g < hi; ++g) {
-    const int np = (sm.live[g] + 1 + page - 1) / page;
-    if (!sm.full[g] && np <= S) { ++wc; wp += np; } else { ++oc; op += np; }
+    s_prefix[g] = off;
+    off += (s_live[g] + 1 + page - 1) / page;
   }
-  int nW, PW, nO, PO;
-  int kw = block_exclusive_scan<BlockSync>(wc, red_i, &nW);
-  int pw = block_exclusive_scan<BlockSync>(wp, red_i, &PW);
-  int ko = block_exclusive_scan<BlockSync>(oc, red_i, &nO);
-  int po = block_exclusive_scan<BlockSync>(op, red_i, &PO);
-  ko += nW;
-  po += PW;
-  for (int g = lo; g < hi; ++g) {
-    const int np = (sm.live[g] + 1 + page - 1) / page;
-    if (!sm.full[g] && np <= S) {
-      sm.order[kw] = g; sm.prefix[kw] = pw; ++kw; pw += np;
-    } else {
-      sm.order[ko] = g; sm.prefix[ko] = po; ++ko; po += np;
-    }
-  }
-  if (tid == 0) sm.prefix[G] = P;
+  if (threadIdx.x == 0) s_prefix[G] = total;
   __syncthreads();
-  // whole heads: CTA c takes those whose first page falls in its share of
-  // the whole-head pages [c*PW/grid, (c+1)*PW/grid)
-  for (int c = tid; c <= grid; c += T) {
-    const long long target = ((long long)c * PW + grid - 1) / grid;  // ceil(c*PW/grid)
-    int a = 0, b = nW;  // first k in [0, nW] with prefix[k] >= target
-    while (a < b) {
-      const int mid = (a + b) >> 1;
-      if (sm.prefix[mid] >= target) b = mid; else a = mid + 1;
-    }
-    sm.W[c] = c == grid ? nW : a;
-  }
-  __syncthreads();
-  // filler: every CTA topped up to S pages, in CTA order; the first
-  // min(fill, pre_pages) of them stream before its whole heads
-  const int perc = (grid + T - 1) / T;
-  const int c0 = min(grid, tid * perc), c1 = min(grid, c0 + perc);
-  int fsum = 0;
-  for (int c = c0; c < c1; ++c)
-    fsum += max(0, S - (sm.prefix[sm.W[c + 1]] - sm.prefix[sm.W[c]]));
-  int ftot;
-  int f = block_exclusive_scan<BlockSync>(fsum, red_i, &ftot);
-  for (int c = c0; c < c1; ++c) {
-    const int fc = max(0, S - (sm.prefix[sm.W[c + 1]] - sm.prefix[sm.W[c]]));
-    const int b = min(f, PO), e = min(f + fc, PO);
-    const int pre = (sm.W[c + 1] > sm.W[c]) ? min(e - b, p.pre_pages) : (e - b);
-    sm.R[2 * c] = PW + b;
-    sm.R[2 * c + 1] = PW + b + pre;
-    f += fc;
-  }
-  if (tid == 0) sm.R[2 * grid] = P;
-  __syncthreads();
-  int ne = 0;
-  for (int c = c0; c < c1; ++c)
-    ne += (sm.R[2 * c + 1] > sm.R[2 * c]) + (sm.R[2 * c + 2] > sm.R[2 * c + 1]);
-  int netot;
-  int e = block_exclusive_scan<BlockSync>(ne, red_i, &netot);
-  for (int c = c0; c < c1; ++c) {
-    sm.Rn[2 * c] = e;
-    e += sm.R[2 * c + 1] > sm.R[2 * c];
-    sm.Rn[2 * c + 1] = e;
-    e += sm.R[2 * c + 2] > sm.R[2 * c + 1];
-  }
-  if (tid == 0) sm.Rn[2 * grid] = netot;
-  __syncthreads();
-  *grid_out = grid;
-  *nW_out = nW;
-  return P;
+  return s_prefix[G];
 }
 
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -682,15 +561,52 @@ __device__ void policy_v3(const DecParams& p, const HeadCtx& hc, float lse, int*
 }
 
 // ---------------------------------------------------------------------------
-// Epilogue of one head: output (+ fused peer stores), then - for evicting
-// heads - the policy.  acc[u] holds output dim tid + u*NC before the 1/l.
+// Epilogue of one head (consumer warps only, named barrier 1).
 template <typename CS, int D, bool kPolicy = true>
-__device__ void head_finish(const DecParams& p, const HeadCtx& hc, float gM, float gl,
-                            const float* acc, int rv, int* hist, int* red_i) {
-  constexpr int NC = CS::kThreads;
+__device__ void head_epilogue(const DecParams& p, const HeadCtx& hc, int nparts, int rv,
+                              int* hist, int* red_i) {
+  constexpr int NC = CS::kThreads, NW = CS::kWarps;
+  const int tid = CS::tid(), lane = tid & 31, warp = tid >> 5;
+  const int g = hc.g, L = hc.L, n = hc.n;
+  // combine the partials of all contributing CTAs; every thread issues its
+  // loads for a batch of parts (max, sum and its output dims) at once, so a
+  // batch costs one L2 round trip
+  const float* parts = p.part + (size_t)g * p.max_parts * (D + 2);
+  constexpr int kB = 8;
   constexpr int DPT = (D + NC - 1) / NC;  // output dims per thread
-  const int tid = CS::tid();
-  const int g = hc.g, n = hc.n;
+  float gM = -INFINITY, gl = 0.f, acc[DPT];
+#pragma unroll
+  for (int u = 0; u < DPT; ++u) acc[u] = 0.f;
+  for (int k0 = 0; k0 < nparts; k0 += kB) {
+    float mk[kB], lk[kB], ok[kB][DPT];
+#pragma unroll
+    for (int b = 0; b < kB; ++b) {
+      const bool v = k0 + b < nparts;
+      const float* pk = parts + (size_t)(k0 + b) * (D + 2);
+      mk[b] = v ? __ldcg(pk + D) : -INFINITY;
+      lk[b] = v ? __ldcg(pk + D + 1) : 0.f;
+#pragma unroll
+      for (int u = 0; u < DPT; ++u) {
+        const int t = tid + u * NC;
+        ok[b][u] = (v && t < D) ? __ldcg(pk + t) : 0.f;
+      }
+    }
+    float newM = gM;
+#pragma unroll
+    for (int b = 0; b < kB; ++b) newM = fmaxf(newM, mk[b]);
+    const float rs = (gM == -INFINITY) ? 0.f : __expf(gM - newM);
+    gl *= rs;
+#pragma unroll
+    for (int u = 0; u < DPT; ++u) acc[u] *= rs;
+#pragma unroll
+    for (int b = 0; b < kB; ++b) {
+      const float w = (mk[b] == -INFINITY) ? 0.f : __expf(mk[b] - newM);
+      gl += w * lk[b];
+#pragma unroll
+      for (int u = 0; u < DPT; ++u) acc[u] += w * ok[b][u];
+    }
+    gM = newM;
+  }
   {
     const float inv = 1.f / gl;
 #pragma unroll
@@ -732,138 +648,53 @@ __device__ void head_finish(const DecParams& p, const HeadCtx& hc, float gM, flo
   if constexpr (kPolicy) policy_v3<CS>(p, hc, lse, hist, red_i, rv);
 }
 
-// Combine the split-K partials of all contributing CTAs.
-template <typename CS, int D>
-__device__ __forceinline__ void combine_parts(const DecParams& p, int g, int nparts, float* gM_out,
-                                              float* gl_out, float* acc) {
-  constexpr int NC = CS::kThreads;
-  const int tid = CS::tid();
-  // every thread issues its loads for a batch of parts (max, sum and its
-  // output dims) at once, so a batch costs one L2 round trip
-  const float* parts = p.part + (size_t)g * p.max_parts * (D + 2);
-  constexpr int kB = 8;
-  constexpr int DPT = (D + NC - 1) / NC;  // output dims per thread
-  float gM = -INFINITY, gl = 0.f;
-#pragma unroll
-  for (int u = 0; u < DPT; ++u) acc[u] = 0.f;
-  for (int k0 = 0; k0 < nparts; k0 += kB) {
-    float mk[kB], lk[kB], ok[kB][DPT];
-#pragma unroll
-    for (int b = 0; b < kB; ++b) {
-      const bool v = k0 + b < nparts;
-      const float* pk = parts + (size_t)(k0 + b) * (D + 2);
-      mk[b] = v ? __ldcg(pk + D) : -INFINITY;
-      lk[b] = v ? __ldcg(pk + D + 1) : 0.f;
-#pragma unroll
-      for (int u = 0; u < DPT; ++u) {
-        const int t = tid + u * NC;
-        ok[b][u] = (v && t < D) ? __ldcg(pk + t) : 0.f;
-      }
-    }
-    float newM = gM;
-#pragma unroll
-    for (int b = 0; b < kB; ++b) newM = fmaxf(newM, mk[b]);
-    const float rs = (gM == -INFINITY) ? 0.f : __expf(gM - newM);
-    gl *= rs;
-#pragma unroll
-    for (int u = 0; u < DPT; ++u) acc[u] *= rs;
-#pragma unroll
-    for (int b = 0; b < kB; ++b) {
-      const float w = (mk[b] == -INFINITY) ? 0.f : __expf(mk[b] - newM);
-      gl += w * lk[b];
-#pragma unroll
-      for (int u = 0; u < DPT; ++u) acc[u] += w * ok[b][u];
-    }
-    gM = newM;
-  }
-  *gM_out = gM;
-  *gl_out = gl;
-}
-
-// Split-K bookkeeping of a launch's page plan: how many CTAs contribute to
-// a head and this CTA's part index.
-// Even plan (SIMT kernel): CTA i owns pages [floor(i*P/grid), floor((i+1)*P/grid)).
-struct EvenPlan {
-  const int* prefix;
-  long long P;
-  int grid;
-  __device__ __forceinline__ void parts(int k, int /*seg*/, int* nparts, int* idx) const {
-    const int own0 = page_owner(prefix[k], P, grid);
-    *nparts = page_owner(prefix[k + 1] - 1, P, grid) - own0 + 1;
-    *idx = blockIdx.x - own0;
-  }
-};
-
-// Publish a CTA's partial (max, sum, o[D]) for head hc from NWC per-warp
+// Publish a CTA's partial (max, sum, o[D]) for head g from NWC per-warp
 // values in s_red / s_ml (group CS), bump the semaphore, and run the
-// epilogue if this CTA is the last contributor.  A head owned by this CTA
-// alone (nparts == 1) is combined straight from shared memory: no partial
-// round trip through L2, no semaphore.  `release` (optional) is arrived on
-// once s_red / s_ml have been consumed.
-template <typename CS, int NWC, int D, bool kPolicy = true, typename Plan>
-__device__ __forceinline__ void publish_head(const DecParams& p, const HeadCtx& hc, const Plan& plan,
+// epilogue if this CTA is the last contributor.  `release` (optional) is
+// arrived on once s_red / s_ml have been consumed.
+template <typename CS, int NWC, int D, bool kPolicy = true>
+__device__ __forceinline__ void publish_head(const DecParams& p, const HeadCtx& hc,
+                                             const int* s_prefix, long long P, int grid,
                                              const float (*s_red)[D], const float (*s_ml)[2],
                                              int* s_last, int rv, int* hist, int* red_i,
                                              uint64_t* release) {
   constexpr int NC = CS::kThreads;
-  constexpr int DPT = (D + NC - 1) / NC;
   const int tid = CS::tid();
   const int g = hc.g;
   CS::sync();
   if (p.trace && tid == 0) p.trace[blockIdx.x * 16 + 8] = gtimer();   // publish start
-  int nparts, idx;
-  plan.parts(hc.k, hc.seg, &nparts, &idx);
+  const int own0 = page_owner(s_prefix[g], P, grid);
+  const int nparts = page_owner(s_prefix[g + 1] - 1, P, grid) - own0 + 1;
+  float* part = p.part + ((size_t)g * p.max_parts + (blockIdx.x - own0)) * (D + 2);
   float M = -INFINITY;
 #pragma unroll
   for (int w = 0; w < NWC; ++w) M = fmaxf(M, s_ml[w][0]);
-  float l = 0.f;
+  for (int t = tid; t < D; t += NC) {
+    float acc = 0.f;
 #pragma unroll
-  for (int w = 0; w < NWC; ++w)
-    if (s_ml[w][0] != -INFINITY) l += s_ml[w][1] * __expf(s_ml[w][0] - M);
-  float acc[DPT];
-#pragma unroll
-  for (int u = 0; u < DPT; ++u) {
-    const int t = tid + u * NC;
-    float a = 0.f;
-    if (t < D) {
-#pragma unroll
-      for (int w = 0; w < NWC; ++w)
-        if (s_ml[w][0] != -INFINITY) a += s_red[w][t] * __expf(s_ml[w][0] - M);
-    }
-    acc[u] = a;
+    for (int w = 0; w < NWC; ++w)
+      if (s_ml[w][0] != -INFINITY) acc += s_red[w][t] * __expf(s_ml[w][0] - M);
+    part[t] = acc;
   }
-  bool run = true;
-  if (nparts == 1) {
-    CS::sync();  // s_red / s_ml consumed
-    if (tid == 0) {
-      if (release) mbar_arrive(release);
-      *s_last = 1;
-    }
-  } else {
-    float* part = p.part + ((size_t)g * p.max_parts + idx) * (D + 2);
+  if (tid == 0) {
+    float l = 0.f;
 #pragma unroll
-    for (int u = 0; u < DPT; ++u) {
-      const int t = tid + u * NC;
-      if (t < D) part[t] = acc[u];
-    }
-    if (tid == 0) {
-      part[D] = M;
-      part[D + 1] = l;
-    }
-    CS::sync();  // the partial is written by the whole group ...
-    if (tid == 0) {  // ... and released to the device by one thread (cumulative)
-      if (release) mbar_arrive(release);
-      int prev;
-      asm volatile("fence.acq_rel.gpu;\n\tatom.add.acq_rel.gpu.global.s32 %0, [%1], 1;"
-                   : "=r"(prev) : "l"(p.counter + g) : "memory");
-      *s_last = (prev == nparts - 1);
-      if (p.trace) p.trace[blockIdx.x * 16 + 9] = gtimer();              // partial released
-    }
-    CS::sync();
-    run = *s_last;
-    if (run) combine_parts<CS, D>(p, g, nparts, &M, &l, acc);
+    for (int w = 0; w < NWC; ++w)
+      if (s_ml[w][0] != -INFINITY) l += s_ml[w][1] * __expf(s_ml[w][0] - M);
+    part[D] = M;
+    part[D + 1] = l;
   }
-  if (run) head_finish<CS, D, kPolicy>(p, hc, M, l, acc, rv, hist, red_i);
+  CS::sync();  // the partial is written by the whole group ...
+  if (tid == 0) {  // ... and released to the device by one thread (cumulative)
+    if (release) mbar_arrive(release);
+    int prev;
+    asm volatile("fence.acq_rel.gpu;\n\tatom.add.acq_rel.gpu.global.s32 %0, [%1], 1;"
+                 : "=r"(prev) : "l"(p.counter + g) : "memory");
+    *s_last = (prev == nparts - 1);
+    if (p.trace) p.trace[blockIdx.x * 16 + 9] = gtimer();                // partial released
+  }
+  CS::sync();
+  if (*s_last) head_epilogue<CS, D, kPolicy>(p, hc, nparts, rv, hist, red_i);
   if (p.trace && tid == 0) p.trace[blockIdx.x * 16 + 10] = gtimer();    // segment finished
 }
 
@@ -1055,8 +886,8 @@ __global__ void __launch_bounds__(SimtShape<T, D>::NW * 32 + 32, 2) k3_decode_si
       for (int e = 0; e < EV; ++e) s_red[warp][sl * EV + e] = o[e];
     }
     if (lane == 0) { s_ml[warp][0] = m_run; s_ml[warp][1] = l_run; }
-    publish_head<NamedSync<NW * 32, 1, 0>, NW, D>(p, hc, EvenPlan{s_prefix, P, grid}, s_red, s_ml,
-                                                  &s_last, LPR, hist, red_i, nullptr);
+    publish_head<NamedSync<NW * 32, 1, 0>, NW, D>(p, hc, s_prefix, P, grid, s_red, s_ml, &s_last,
+                                                  LPR, hist, red_i, nullptr);
     m_run = -INFINITY;
     l_run = 0.f;
 #pragma unroll
@@ -1136,18 +967,9 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
   using ES = NamedSync<S::NE * 32, 2, S::EFIRST>;
 
   const int G = p.G;
-  PlanSmem sm;
-  sm.prefix = reinterpret_cast<int*>(smem + ST * S::STAGE_B);
-  sm.order = sm.prefix + (G + 1);
-  sm.live = sm.order + G;
-  sm.W = sm.live + G;
-  sm.R = sm.W + (kMaxGrid + 1);
-  sm.Rn = sm.R + (2 * kMaxGrid + 1);
-  sm.full = reinterpret_cast<uint8_t*>(sm.Rn + (2 * kMaxGrid + 1));
-  const int* s_prefix = sm.prefix;
-  const int* s_order = sm.order;
-  const int* s_live = sm.live;
-  const uint8_t* s_full = sm.full;
+  int* s_prefix = reinterpret_cast<int*>(smem + ST * S::STAGE_B);
+  int* s_live = s_prefix + (G + 1);
+  uint8_t* s_full = reinterpret_cast<uint8_t*>(s_live + G);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   AKV_TRACE(0);
   if (tid == 0) {
@@ -1178,56 +1000,41 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
     early = (p.flags & AKV_DECODE_CHAINED) && step > 0;
     if (!early) grid_dep_wait();
   }
-  // This CTA's work: three page ranges of the flattened page order, in
-  // stream order - pre filler, whole heads, post filler - each with the
-  // order index of its first head.  Kept in shared memory: the consumer
-  // loop runs at the register limit.
-  __shared__ struct {
-    int rb[3], re[3], rk[3];
-    int last_r, k_last, nW, grid;
-  } s_work;
-  {
-    int grid, nW;
-    plan_mixed(p, PAGE, step, sm, red_i, &grid, &nW);
-    if ((int)blockIdx.x >= grid) return;
-    if (tid == 0) {
-      const int c = blockIdx.x;
-      s_work.rb[0] = sm.R[2 * c]; s_work.re[0] = sm.R[2 * c + 1];
-      s_work.rb[1] = s_prefix[sm.W[c]]; s_work.re[1] = s_prefix[sm.W[c + 1]];
-      s_work.rb[2] = sm.R[2 * c + 1]; s_work.re[2] = sm.R[2 * c + 2];
-      int last_r = -1;
-      for (int r = 0; r < 3; ++r) {
-        s_work.rk[r] = s_work.re[r] > s_work.rb[r] ? head_of_page(s_prefix, G, s_work.rb[r]) : G;
-        if (s_work.re[r] > s_work.rb[r]) last_r = r;
-      }
-      // the consumers publish the CTA's last segment themselves when it
-      // belongs to a full-cache head (no policy to run): its order index
-      int k_last = -1;
-      if (last_r >= 0) {
-        const int kl = head_of_page(s_prefix, G, s_work.re[last_r] - 1);
-        if (p.consumer_tail && s_full[s_order[kl]]) k_last = kl;
-      }
-      s_work.last_r = last_r;
-      s_work.k_last = k_last;
-      s_work.nW = nW;
-      s_work.grid = grid;
-    }
-    __syncthreads();
-  }
+  const long long P = plan_pages_bound(p, PAGE, step, s_prefix, s_live, s_full, red_i);
   AKV_TRACE(1);
+  const int grid = (int)(P < (long long)gridDim.x ? P : (long long)gridDim.x);
+  if ((int)blockIdx.x >= grid) return;
+  const long long pbeg = (long long)blockIdx.x * P / grid;
+  const long long pend = (long long)(blockIdx.x + 1) * P / grid;
+  const int g0 = head_of_page(s_prefix, G, pbeg);
 
   if (warp == NW) {  // ---------------- producer ----------------
     if (lane == 0) {
       const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
       bool waited = !early;
-      int stage = 0, kl = -1, L = 0, g = 0;
+      int g = g0, stage = 0, gl = -1, L = 0;
       uint32_t phase = 0;
-      for (int r = 0; r < 3; ++r)
-      for (int pg = s_work.rb[r], pend = s_work.re[r], k = s_work.rk[r]; pg < pend; ++pg) {
-        while (pg >= s_prefix[k + 1]) ++k;
-        if (k != kl) {
-          kl = k;
-          g = s_order[k];
+      // L2 prefetch cursor: the pages just beyond the shared-memory ring go
+      // to L2 early (coherent, so safe before the previous step drains),
+      // raising the bytes in flight per CTA beyond what the ring can hold
+      long long pf = pbeg + ST;
+      int gpf = g0;
+      for (long long pg = pbeg; pg < pend; ++pg) {
+        for (const long long lim = min(pend, pg + ST + p.l2_prefetch); pf < lim; ++pf) {
+          while (pf >= s_prefix[gpf + 1]) ++gpf;
+          const int s0 = (int)(pf - s_prefix[gpf]) * PAGE;
+          if (s0 <= s_live[gpf]) {
+            const int row0 = (int)(p.seg_off[gpf] + s0);
+#pragma unroll
+            for (int bx = 0; bx < S::NBOX; ++bx) {
+              tma_prefetch_l2_2d(&tmK, bx * 64, row0);
+              tma_prefetch_l2_2d(&tmV, bx * 64, row0);
+            }
+          }
+        }
+        while (pg >= s_prefix[g + 1]) ++g;
+        if (g != gl) {
+          gl = g;
           if (s_full[g]) {
             L = s_live[g];
           } else {
@@ -1235,7 +1042,7 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
             L = live_after_wait(p, g);
           }
         }
-        const int slot0 = (int)(pg - s_prefix[k]) * PAGE;
+        const int slot0 = (int)(pg - s_prefix[g]) * PAGE;
         const int rows = max(0, min(PAGE, L - slot0));
         const bool has_new = (L >= slot0 && L < slot0 + PAGE);
         // the previous step wrote row L-1 of a full head; a page holding it waits
@@ -1276,28 +1083,23 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
     // step until it completes; once it has, dependents may launch
     grid_dep_wait();
     if (warp == NW + 1 && lane == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    // one published segment per head touched by this CTA's work, in order:
-    // the whole heads, then the heads its filler range overlaps
+    // one published segment per head touched by this CTA's page range, in order
     int pub_n = 0;
-    const MixedPlan plan{s_prefix, sm.R, sm.Rn, s_work.nW, s_work.grid};
-    const int k_last = s_work.k_last, last_r = s_work.last_r;
-    // one published segment per (range, head) of this CTA's work, in order
-    for (int r = 0; r < 3; ++r) {
-      const int pend = s_work.re[r];
-      for (int k = s_work.rk[r]; k < G && s_prefix[k] < pend; ++k) {
-        if (s_prefix[k + 1] == s_prefix[k]) continue;  // head without pages
-        if (r == last_r && k == k_last && s_prefix[k + 1] >= pend) break;
-        const int slot = pub_n & 1;
-        mbar_wait(&pub_full[slot], (pub_n >> 1) & 1);
-        const HeadCtx hc = s_pub[slot].ctx;
-        publish_head<ES, NW, D>(p, hc, plan, s_pub[slot].red, s_pub[slot].ml, &s_last, RB / 16,
-                                hist, red_i, &pub_empty[slot]);
-        if (s_last && p.trace && ES::tid() == 0) {
-          atomicAdd(&p.trace[blockIdx.x * 16 + 5], 1ull);               // epilogues run
-          if (hc.freq) atomicAdd(&p.trace[blockIdx.x * 16 + 6], 1ull);  // frequent ones
-        }
-        ++pub_n;
+    for (int g = g0; g < G && s_prefix[g] < pend; ++g) {
+      if (s_prefix[g + 1] == s_prefix[g]) continue;  // head without pages
+      // the consumers publish the CTA's last segment themselves when it
+      // belongs to a full-cache head (no policy to run)
+      if (p.consumer_tail && s_prefix[g + 1] >= pend && (p.atoms[g] & AKV_ATOM_FULL)) break;
+      const int slot = pub_n & 1;
+      mbar_wait(&pub_full[slot], (pub_n >> 1) & 1);
+      const HeadCtx hc = s_pub[slot].ctx;
+      publish_head<ES, NW, D>(p, hc, s_prefix, P, grid, s_pub[slot].red, s_pub[slot].ml, &s_last,
+                              RB / 16, hist, red_i, &pub_empty[slot]);
+      if (s_last && p.trace && ES::tid() == 0) {
+        atomicAdd(&p.trace[blockIdx.x * 16 + 5], 1ull);               // epilogues run
+        if (hc.freq) atomicAdd(&p.trace[blockIdx.x * 16 + 6], 1ull);  // frequent ones
       }
+      ++pub_n;
     }
     if (p.trace && ES::tid() == 0) p.trace[blockIdx.x * 16 + 4] = gtimer();
     return;
@@ -1306,42 +1108,29 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
   // ---------------- consumers ----------------
   const int gq = lane >> 2, qq = lane & 3;  // mma fragment coordinates
   int pub_n = 0;
-  int stage = 0;
+  int g = g0, stage = 0;
   uint32_t phase = 0;
-  // the warp's current head, kept in shared memory (read per page; the
-  // loop runs at the register limit)
-  __shared__ HeadCtx s_hcw[NW];
-  HeadCtx& hc = s_hcw[warp];
-  if (lane == 0) { hc.g = -1; hc.k = -1; hc.seg = -1; }
-  __syncwarp();
+  HeadCtx hc;
+  hc.g = -1;
   float m_run = -INFINITY, l_run = 0.f;
   float o[NK][4];
 #pragma unroll
   for (int t = 0; t < NK; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
 
-  bool first = true;
-  for (int r = 0; r < 3; ++r)
-  for (int pg = s_work.rb[r], pend = s_work.re[r], k = s_work.rk[r]; pg < pend; ++pg) {
-    while (pg >= s_prefix[k + 1]) ++k;
-    if (k != hc.k || r != hc.seg) {
-      const int g = s_order[k];
+  for (long long pg = pbeg; pg < pend; ++pg) {
+    while (pg >= s_prefix[g + 1]) ++g;
+    if (g != hc.g) {
       int Lh = s_live[g];
       if (!s_full[g]) {  // evicting head: its live count comes from the previous step
         if (early) grid_dep_wait();
         Lh = live_after_wait(p, g);
       }
-      HeadCtx t;
-      load_head(p, g, Lh, t);
-      t.k = k;
-      t.seg = r;
-      __syncwarp();
-      if (lane == 0) hc = t;
-      __syncwarp();
+      load_head(p, g, Lh, hc);
     }
     const int L = hc.L, n = hc.n;
-    const int slot0 = (int)(pg - s_prefix[k]) * PAGE;
+    const int slot0 = (int)(pg - s_prefix[g]) * PAGE;
     mbar_wait(&full_bar[stage], phase);
-    if (first) { AKV_TRACE(2); first = false; }
+    if (pg == pbeg) AKV_TRACE(2);
     uint8_t* st = smem + stage * S::STAGE_B;
     const uint32_t kbase = smem_u32(st), vbase = smem_u32(st + kPageBytes);
     const int* mpage = reinterpret_cast<const int*>(st + 2 * kPageBytes);
@@ -1451,12 +1240,9 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
     if (lane == 0) mbar_arrive(&empty_bar[stage]);
     if (++stage == ST) { stage = 0; phase ^= 1; }
 
-    if (!(pg + 1 == pend || pg + 1 == s_prefix[k + 1])) continue;
+    if (!((pg + 1 == pend) || (pg + 1 == s_prefix[g + 1]))) continue;
     l_run = warp_allreduce(l_run, [](float a, float b) { return a + b; });
-    // the CTA's last page: the end of the filler range, or of the whole
-    // heads when the filler range is empty
-    const bool last = pg + 1 == pend && r == s_work.last_r;
-    if (k == s_work.k_last && last) {
+    if (p.consumer_tail && pg + 1 == pend && (hc.atoms & AKV_ATOM_FULL)) {
       // The CTA's last segment, of a full-cache head: publish it from the
       // consumer warps, in parallel with the epilogue warps finishing the
       // previous segment (that serialisation was the step's tail).  Every
@@ -1480,9 +1266,8 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
       }
       if (lane == 0) { mls[warp][0] = m_run; mls[warp][1] = l_run; }
       AKV_TRACE(3);
-      publish_head<CSync, NW, D, false>(p, hc, MixedPlan{s_prefix, sm.R, sm.Rn, s_work.nW, s_work.grid},
-                                        red, mls, scratch_i + 300, RB / 16, scratch_i,
-                                        scratch_i + 256, nullptr);
+      publish_head<CSync, NW, D, false>(p, hc, s_prefix, P, grid, red, mls, scratch_i + 300,
+                                        RB / 16, scratch_i, scratch_i + 256, nullptr);
       return;
     }
     // hand the segment to the epilogue warps and keep streaming
@@ -1506,7 +1291,7 @@ __global__ void __launch_bounds__(MmaShape<D>::THREADS, 2)
       if (lane == 0) mbar_arrive(&pub_full[slot]);
       ++pub_n;
     }
-    if (last) AKV_TRACE(3);
+    if (pg + 1 == pend) AKV_TRACE(3);
     m_run = -INFINITY;
     l_run = 0.f;
 #pragma unroll
@@ -1524,7 +1309,7 @@ static int env_int(const char* name, int dflt) {
 // Decode grid: AKV_K3_GRID CTAs if set (tuning), else 2 per SM
 static int k3_grid(int sms) {
   static const int v = env_int("AKV_K3_GRID", 0);
-  return min(kMaxGrid, v > 0 ? v : 2 * sms);
+  return v > 0 ? v : 2 * sms;
 }
 unsigned long long* g_dec_trace = nullptr;  // set by akv_debug_set_decode_trace
 // consumers publish the CTA's last full-cache segment (AKV_K3_CONSUMER_TAIL, tuning)
@@ -1537,12 +1322,6 @@ static int k3_l2_prefetch() {
   // measured at config 1: 0 best (2: +0.6 us, 4: +1.4, 8: +4.1)
   static const int v = env_int("AKV_K3_L2_PREFETCH", 0) > 0 ? env_int("AKV_K3_L2_PREFETCH", 0) : 0;
   return v;
-}
-
-// filler pages a CTA streams before its whole heads (AKV_K3_PRE_PAGES, tuning)
-static int k3_pre_pages() {
-  static const int v = env_int("AKV_K3_PRE_PAGES", 4);
-  return v < 0 ? 0 : v;
 }
 
 static std::atomic<int> g_num_sms[kMaxDevices];
@@ -1637,10 +1416,7 @@ static cudaError_t launch_mma(const DecParams& p, int64_t total_slots, cudaStrea
   }
   auto k3 = k3_decode_mma<D, 3>;
   auto k2 = k3_decode_mma<D, 2>;
-  // page plan (PlanSmem): prefix, order, live bound, full flag per head +
-  // three per-CTA arrays
-  auto plan_bytes = [](int G) { return (size_t)(3 * G + 1) * 4 + (size_t)(5 * kMaxGrid + 3) * 4 + G; };
-  const size_t plan = plan_bytes(kMaxHeads);
+  const size_t plan = (size_t)(2 * kMaxHeads + 1) * 4 + kMaxHeads;
   // per-device launch facts: the attribute opt-ins and the shared-memory
   // budget that decides whether a 3-stage ring keeps two CTAs per SM
   struct Facts { size_t static3, per_sm, reserve; };
@@ -1671,7 +1447,7 @@ static cudaError_t launch_mma(const DecParams& p, int64_t total_slots, cudaStrea
   const Facts& f = facts[dev];
   int sms;
   if ((e = num_sms(&sms))) return e;
-  const size_t plan_g = plan_bytes(p.G);
+  const size_t plan_g = (size_t)(2 * p.G + 1) * 4 + p.G;
   const size_t smem3 = 1024 + (size_t)3 * S::STAGE_B + plan_g;
   // Two ring stages by default: measured at least as fast as three at every
   // size (c1 29.44 -> 29.26 us/step; B*H 128..512 likewise) and they keep two
@@ -1788,7 +1564,7 @@ extern "C" int akv_decode_step(const akv_decode_args* a, void* stream) {
                 w.part + g0 * w.max_parts * (a->d + 2), w.logit, w.counter + g0, w.max_parts, scale,
                 g_dec_trace, a->pos_dev, a->flags, at(a->lse_out_dev, g0), a->peer_out_dev,
                 a->n_peers, a->peer_ld, a->peer_col0 + (int64_t)b0 * a->peer_ld,
-                a->dtype == AKV_DTYPE_BF16, k3_l2_prefetch(), k3_consumer_tail(), k3_pre_pages()};
+                a->dtype == AKV_DTYPE_BF16, k3_l2_prefetch(), k3_consumer_tail()};
     if (a->dtype == AKV_DTYPE_BF16) {
       switch (a->d) {
         case 16: e = launch_simt<__nv_bfloat16, 16>(p, st); break;

@@ -65,6 +65,8 @@ def regime(name, T, reps=3):
         lib.akv_debug_set_decode_trace(None)
     torch.cuda.synchronize()
     tr = buf.view(-1, 16).cpu().numpy().astype(np.float64)
+    if os.environ.get("AKV_TRACE_DUMP"):
+        np.save(f"{os.environ['AKV_TRACE_DUMP']}_{name}_{T:g}.npy", buf.view(-1, 16).cpu().numpy())
     ok = tr[:, 4] > 0
     t0 = tr[ok, 0].min()
     rel = (tr[ok] - t0) / 1e3
@@ -81,6 +83,11 @@ def regime(name, T, reps=3):
             "frequent_epilogues": int(tr[ok, 6].sum()), "radix_fallbacks": int(tr[ok, 7].sum()),
             "isolated_step_us": float(rel[:, 4].max()),
             "plan_us_median": float(np.median(rel[:, 1] - rel[:, 0])),
+            # slots 11-15: plan phase (-DAKV_TRACE_PLAN) or FREQUENT epilogue phase
+            # (-DAKV_TRACE_EPI) cycle stamps, relative to slot 11
+            "phase_cycles_median": [float(np.median((tr[:, j] - tr[:, 11])[(tr[:, 11] > 0) & (tr[:, j] > 0)]))
+                                    if ((tr[:, 11] > 0) & (tr[:, j] > 0)).any() else None
+                                    for j in (12, 13, 14, 15)],
             "first_page_us_median": float(np.median(rel[:, 2] - rel[:, 0])),
             "last_page_us_median": float(np.median(rel[:, 3])),
             "tail_after_last_page_us": [float(np.percentile((rel[:, 4] - rel[:, 3])[tr[ok, 3] > 0], p))
