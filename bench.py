@@ -452,7 +452,7 @@ def bench_ours(args):
         print(json.dumps(line), flush=True)
 
 
-def _c4_session(w, T, R, peaks):
+def _extra_session(w, T, R, peaks):
     """One warm + one timed config-4 session on this rank's shard; times are
     the max over ranks."""
     import torch
@@ -499,7 +499,7 @@ def bench_extras(T, dev, peaks):
 
     out = {}
     w = config4()
-    r = _c4_session(w, T, _One(dev), peaks)
+    r = _extra_session(w, T, _One(dev), peaks)
     N, D = w.N, w.D
     out["c4"] = {
         "workload": f"long context: B={w.B} H={w.H} d={w.d} N={N} D={D} bf16, T={T:g}",
@@ -509,6 +509,25 @@ def bench_extras(T, dev, peaks):
         "decode_us_per_step": r["dec_ms"] * 1e3 / D, "decode_achieved_gbs": r["gbs"],
         "decode_frac_of_hbm_peak": r["frac"],
         "pruned_ratio_end": 1.0 - r["retained"] / float(w.B * w.H * (N + D)),
+        "policies": r["policies"],
+    }
+    # the FREQUENT-heavy regime at config-1 shapes (the paper's compression
+    # regime): ~3/4 of the heads evict through the score update + top-k at
+    # every step; K3 against its algorithmic bytes incl. 16 B/slot of scores
+    from paper_2310_01801_b200.workloads import config1_frequent
+
+    wf = config1_frequent()
+    Tf = wf.thresholds[0]
+    r = _extra_session(wf, Tf, _One(dev), peaks)
+    fam_freq = sum(v for k, v in r["policies"].items() if "frequent" in k)
+    out["c1_frequent"] = {
+        "workload": f"config-1 shapes B={wf.B} H={wf.H} d={wf.d} N={wf.N} D={wf.D} bf16, a sink "
+                    f"on every head (U[9.6, 11.0] logits), T={Tf:g}: {fam_freq} of {wf.B * wf.H} "
+                    "heads FREQUENT",
+        "session_tok_s": wf.B * wf.D / ((r["enc_ms"] + r["dec_ms"]) * 1e-3),
+        "decode_us_per_step": r["dec_ms"] * 1e3 / wf.D, "decode_achieved_gbs": r["gbs"],
+        "decode_frac_of_hbm_peak": r["frac"],
+        "pruned_ratio_end": 1.0 - r["retained"] / float(wf.B * wf.H * (wf.N + wf.D)),
         "policies": r["policies"],
     }
     out["c2"] = _c2_decode(T, dev, peaks)
@@ -546,7 +565,7 @@ def bench_extras_multi(T, R, peaks, args, rank0_line):
 
     w4 = config4()
     sh = head_shard(w4.B, w4.H, R.world, R.rank)
-    r = _c4_session(w4.heads(sh.h0, sh.h1), T, R, peaks)
+    r = _extra_session(w4.heads(sh.h0, sh.h1), T, R, peaks)
     enc, decm = R.max(r["enc_ms"], r["dec_ms"])
     ranks = R.gather({k: r[k] for k in ("enc_ms", "dec_ms", "gbs", "frac", "retained", "costs")})
     # decode cost per head (kept + D live rows), global (b, h) order

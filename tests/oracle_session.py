@@ -31,14 +31,15 @@ def _workloads():
 
 
 def run_heads(job):
-    """job = (seed, B, H, N, D, T, [(b, h), ...]).  Returns a list of dicts."""
+    """job = (config name, seed, B, H, N, D, T, [(b, h), ...]).  Returns a
+    list of dicts."""
     from threadpoolctl import threadpool_limits
 
     from oracle import akv_oracle as O
 
-    seed, B, H, N, D, T, heads = job
+    name, seed, B, H, N, D, T, heads = job
     W = _workloads()
-    w = W.config1(seed=seed, B=B, H=H, N=N, D=D)
+    w = W.CONFIGS[name](seed=seed, B=B, H=H, N=N, D=D)
     lut = W.class_lut()
     fam = O.default_family(w.r_l, w.r_f)
     out = []

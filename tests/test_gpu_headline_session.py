@@ -85,18 +85,23 @@ def _oracle(w, T):
 
     units = [(b, h) for b in range(w.B) for h in range(w.H)]
     workers = max(1, min(len(os.sched_getaffinity(0)), 32))
-    jobs = [(w.seed, w.B, w.H, w.N, w.D, T, units[i::workers]) for i in range(workers)]
+    jobs = [(w.name, w.seed, w.B, w.H, w.N, w.D, T, units[i::workers]) for i in range(workers)]
     with mp.get_context("spawn").Pool(workers) as pool:
         parts = pool.map(oracle_session.run_heads, jobs)
     by = {(r["b"], r["h"]): r for part in parts for r in part}
     return [by[u] for u in units]
 
 
-@pytest.mark.parametrize("T", [0.95, 0.98, 0.99])
-def test_headline_session_every_head_every_step(T):
-    from paper_2310_01801_b200.workloads import config1
+@pytest.mark.parametrize("name,T", [("c1", 0.95), ("c1", 0.98), ("c1", 0.99),
+                                    ("c1_frequent", 0.98)])
+def test_headline_session_every_head_every_step(name, T):
+    """c1: the headline workload at each T of the sweep.  c1_frequent:
+    config-1 shapes with a sink on every head - about 200 of the 256 heads
+    evict through the frequent score update and top-k at every one of the
+    512 steps (the K3 FREQUENT-heavy measurement's workload)."""
+    from paper_2310_01801_b200.workloads import CONFIGS
 
-    w = config1(seed=1)
+    w = CONFIGS[name]()
     res, enc, kept, outs = _gpu_session(w, T)
     ref = _oracle(w, T)
     G, D = w.B * w.H, w.D
@@ -130,7 +135,7 @@ def test_headline_session_every_head_every_step(T):
     fam = res.family
     pol = np.bincount(res.choice[:, 0], minlength=len(fam))
     evicting = int(sum(1 for g in keep if not fam[res.choice[g, 0]].is_full))
-    print(f"headline T={T}: {len(keep)} of {G} heads compared over {D} steps "
+    print(f"{name} T={T}: {len(keep)} of {G} heads compared over {D} steps "
           f"({len(keep) * D} head-steps, {evicting} evicting heads), 0 policy / kept-set "
           f"mismatches; near-T heads listed separately: {near_t} (of which policy and every kept set agree anyway: {near_t_agree}); max |o - o_ref| / max|o_ref| "
           f"= {worst:.2e}; policies {dict((str(fam[i]), int(pol[i])) for i in range(len(fam)) if pol[i])}")
