@@ -297,6 +297,13 @@ __global__ void __launch_bounds__(kTcThreads, 2)
 }
 
 // ---------------------------------------------------------------------------
+// Pass 2, paired like pass 1: CTA (x, g) processes key tiles x and
+// ntiles-1-x of head g (one when they coincide), ntiles+1 query tiles in
+// all - uniform work per CTA, half the CTA setups (TMEM allocation,
+// barriers, descriptor prefetch, first TMA round trip).  The first item
+// (key tile x, ntiles-x query tiles) is the heavier one.
+constexpr size_t kTcSmemCol = kTcSmem + (size_t)(32 * kEpiWarps / 16) * 128 * 4;  // + out_part scratch
+
 __global__ void __launch_bounds__(kTcThreads, 2)
     k1tc_colsum(const __grid_constant__ TcParams p, const __grid_constant__ CUtensorMap tmQ,
                 const __grid_constant__ CUtensorMap tmK) {
@@ -304,17 +311,21 @@ __global__ void __launch_bounds__(kTcThreads, 2)
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sK = smem;
   uint8_t* sQ = smem + kTileB;
-  __shared__ __align__(8) uint64_t k_full, q_full[kRing], q_empty[kRing], acc_full[2], acc_empty[2];
+  float* s_red = reinterpret_cast<float*>(smem + (1 + kRing) * kTileB);  // [RG][128]
+  __shared__ __align__(8) uint64_t k_full, k_empty, q_full[kRing], q_empty[kRing], acc_full[2],
+      acc_empty[2];
   __shared__ uint32_t s_tmem;
   __shared__ __align__(16) float s_col[2][kTT];
   __shared__ float s_lastp[kTT];
   const int ntiles = (p.N + kTT - 1) / kTT;
   const int g = blockIdx.y, h = g % p.H, b = g / p.H;
-  const int kt = blockIdx.x;  // key tile 0 sees the most query tiles: first
-  const int nq = ntiles - kt;
+  const int x = blockIdx.x;
+  const int nitems = (ntiles - 1 - x == x) ? 1 : 2;
+  auto item_kt = [&](int j) { return j == 0 ? x : ntiles - 1 - x; };  // heavier first
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     mbar_init(&k_full, 1);
+    mbar_init(&k_empty, 1);
     for (int s = 0; s < kRing; ++s) { mbar_init(&q_full[s], 1); mbar_init(&q_empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&acc_full[a], 1); mbar_init(&acc_empty[a], kEpiWarps); }
     mbar_fence_init();
@@ -330,30 +341,40 @@ __global__ void __launch_bounds__(kTcThreads, 2)
   if (warp == 0) {  // ---------------- TMA producer ----------------
     if (lane == 0) {
       const uint64_t pol_k = policy_evict_first(), pol_q = policy_evict_last();
-      const int rk = (int)((int64_t)g * p.ld + (int64_t)kt * kTT);
-      mbar_arrive_expect_tx(&k_full, kTileB);
-      tma_load_2d(sK, &tmK, 0, rk, &k_full, pol_k);
-      tma_load_2d(sK + kBoxB, &tmK, 64, rk, &k_full, pol_k);
-      for (int i = 0; i < nq; ++i) {
-        const int s = i % kRing;
-        mbar_wait(&q_empty[s], ((i / kRing) & 1) ^ 1);
-        mbar_arrive_expect_tx(&q_full[s], kTileB);
-        const int rq = (int)((int64_t)g * p.ld + (int64_t)(kt + i) * kTT);
-        tma_load_2d(sQ + s * kTileB, &tmQ, 0, rq, &q_full[s], pol_q);
-        tma_load_2d(sQ + s * kTileB + kBoxB, &tmQ, 64, rq, &q_full[s], pol_q);
+      int t = 0;
+      for (int j = 0; j < nitems; ++j) {
+        const int kt = item_kt(j), nq = ntiles - kt;
+        const int rk = (int)((int64_t)g * p.ld + (int64_t)kt * kTT);
+        mbar_wait(&k_empty, (j & 1) ^ 1);  // the previous item's MMAs have read sK
+        mbar_arrive_expect_tx(&k_full, kTileB);
+        tma_load_2d(sK, &tmK, 0, rk, &k_full, pol_k);
+        tma_load_2d(sK + kBoxB, &tmK, 64, rk, &k_full, pol_k);
+        for (int i = 0; i < nq; ++i, ++t) {
+          const int s = t % kRing;
+          mbar_wait(&q_empty[s], ((t / kRing) & 1) ^ 1);
+          mbar_arrive_expect_tx(&q_full[s], kTileB);
+          const int rq = (int)((int64_t)g * p.ld + (int64_t)(kt + i) * kTT);
+          tma_load_2d(sQ + s * kTileB, &tmQ, 0, rq, &q_full[s], pol_q);
+          tma_load_2d(sQ + s * kTileB + kBoxB, &tmQ, 64, rq, &q_full[s], pol_q);
+        }
       }
     }
   } else if (warp == 1) {  // ---------------- MMA issuer ----------------
     if (lane == 0) {
-      mbar_wait(&k_full, 0);
-      for (int i = 0; i < nq; ++i) {
-        const int s = i % kRing, a = i & 1;
-        mbar_wait(&q_full[s], (i / kRing) & 1);
-        mbar_wait(&acc_empty[a], ((i >> 1) & 1) ^ 1);
-        tc_fence_after();
-        mma_tile(tmem + a * kTT, sK, sQ + s * kTileB);  // S^T: keys on TMEM lanes
-        umma_commit(&q_empty[s]);
-        umma_commit(&acc_full[a]);
+      int t = 0;
+      for (int j = 0; j < nitems; ++j) {
+        const int nq = ntiles - item_kt(j);
+        mbar_wait(&k_full, j & 1);
+        for (int i = 0; i < nq; ++i, ++t) {
+          const int s = t % kRing, a = t & 1;
+          mbar_wait(&q_full[s], (t / kRing) & 1);
+          mbar_wait(&acc_empty[a], ((t >> 1) & 1) ^ 1);
+          tc_fence_after();
+          mma_tile(tmem + a * kTT, sK, sQ + s * kTileB);  // S^T: keys on TMEM lanes
+          umma_commit(&q_empty[s]);
+          umma_commit(&acc_full[a]);
+        }
+        umma_commit(&k_empty);
       }
     }
   } else {  // ---------------- epilogue (warps 2-9) ----------------
@@ -363,159 +384,163 @@ __global__ void __launch_bounds__(kTcThreads, 2)
     const int et = threadIdx.x - 64;
     const int half = et >> 7;  // column group: query columns [kCols*half, kCols*(half+1)) of a tile
     const int kl = quarter * 32 + lane;
-    const int key = kt * kTT + kl;
     const float sl2 = p.scale * kLog2e;
     const float slope_l2 = (p.slope ? p.slope[h] : 0.f) * kLog2e;
     const float sink_l2 = (p.sink ? p.sink[h] : 0.f) * kLog2e;
     const uint8_t* cls = p.cls + (size_t)b * p.cls_ld;
     const float* lse = p.lse + (size_t)g * p.N;
-    // per-key term: sink on a special key, + slope * key.  Without a slope
-    // the key term is a constant factor of the key's column and is applied
-    // to the tile sums (kfac) instead of inside every exponential.
-    const float ksink = key < p.N && cls[key] == AKV_CLS_SPECIAL ? sink_l2 : 0.f;
     const bool slope_on = slope_l2 != 0.f;
-    const float kterm = ksink + slope_l2 * (float)key;
-    const float kfac = fast_exp2(ksink);
-    double dsum = 0.0, dsq = 0.0;
-    float lastp = 0.f;
     const int qlast = p.N - 1;
-    float lnext = 0.f;
     // the row pass (programmatic predecessor) must be complete before lse is
     // read; the producer and MMA warps run ahead meanwhile
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (et < kTT) lnext = kt * kTT + et < p.N ? lse[kt * kTT + et] : 0.f;
-    for (int i = 0; i < nq; ++i) {
-      const int a = i & 1;
-      const int qt = kt + i;
-      if (et < kTT) {  // per-query term of this tile: -lse_q * log2e - slope * q
-        const int q = qt * kTT + et;
-        s_col[a][et] = -lnext * kLog2e - slope_l2 * (float)q;
-        const int qn = q + kTT;
-        lnext = (i + 1 < nq && qn < p.N) ? lse[qn] : 0.f;
-      }
-      EpiSync::sync();
-      mbar_wait(&acc_full[a], (i >> 1) & 1);
-      tc_fence_after();
-      float v[kCols];
-      tmem_ld_cols(tmem + ((uint32_t)(quarter * 32) << 16) + a * kTT + half * kCols, v);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[a]);
-      // diagonal tile (causal mask), ragged tail (q >= N) and the tile holding row N-1
-      const bool masked = (i == 0) || ((qt + 1) * kTT > p.N) || (qt == qlast / kTT);
-      const float* ct = &s_col[a][half * kCols];
-      float ts[4] = {0.f, 0.f, 0.f, 0.f}, tq[4] = {0.f, 0.f, 0.f, 0.f};
-      if (masked) {
-        const int q0 = qt * kTT + half * kCols;
-#pragma unroll
-        for (int c = 0; c < kCols; ++c) {
-          float pr = fast_exp2(fmaf(v[c], sl2, kterm + ct[c]));
-          const int q = q0 + c;
-          if (q < key || q >= p.N) pr = 0.f;
-          if (q == qlast) lastp = pr;
-          ts[c & 3] += pr;
-          tq[c & 3] = fmaf(pr, pr, tq[c & 3]);
+    int t = 0;
+    for (int j = 0; j < nitems; ++j) {
+      const int kt = item_kt(j), nq = ntiles - kt;
+      const int key = kt * kTT + kl;
+      // per-key term: sink on a special key, + slope * key.  Without a slope
+      // the key term is a constant factor of the key's column and is applied
+      // to the tile sums (kfac) instead of inside every exponential.
+      const float ksink = key < p.N && cls[key] == AKV_CLS_SPECIAL ? sink_l2 : 0.f;
+      const float kterm = ksink + slope_l2 * (float)key;
+      const float kfac = fast_exp2(ksink);
+      double dsum = 0.0, dsq = 0.0;
+      float lastp = 0.f;
+      float lnext = 0.f;
+      if (et < kTT) lnext = kt * kTT + et < p.N ? lse[kt * kTT + et] : 0.f;
+      for (int i = 0; i < nq; ++i, ++t) {
+        const int a = t & 1;
+        const int qt = kt + i;
+        if (et < kTT) {  // per-query term of this tile: -lse_q * log2e - slope * q
+          const int q = qt * kTT + et;
+          s_col[a][et] = -lnext * kLog2e - slope_l2 * (float)q;
+          const int qn = q + kTT;
+          lnext = (i + 1 < nq && qn < p.N) ? lse[qn] : 0.f;
         }
-        dsum += (double)((ts[0] + ts[1]) + (ts[2] + ts[3]));
-        dsq += (double)((tq[0] + tq[1]) + (tq[2] + tq[3]));
-      } else if (slope_on) {
+        EpiSync::sync();
+        mbar_wait(&acc_full[a], (t >> 1) & 1);
+        tc_fence_after();
+        float v[kCols];
+        tmem_ld_cols(tmem + ((uint32_t)(quarter * 32) << 16) + a * kTT + half * kCols, v);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[a]);
+        // diagonal tile (causal mask), ragged tail (q >= N) and the tile holding row N-1
+        const bool masked = (i == 0) || ((qt + 1) * kTT > p.N) || (qt == qlast / kTT);
+        const float* ct = &s_col[a][half * kCols];
+        float ts[4] = {0.f, 0.f, 0.f, 0.f}, tq[4] = {0.f, 0.f, 0.f, 0.f};
+        if (masked) {
+          const int q0 = qt * kTT + half * kCols;
 #pragma unroll
-        for (int c = 0; c < kCols; c += 4) {
-          const float4 t = *reinterpret_cast<const float4*>(ct + c);
-          const float tt[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float x = fmaf(v[c + u], sl2, kterm + tt[u]);
-            const float pr = exp2_mixed(x, u);
-            ts[u] += pr;
-            tq[u] = fmaf(pr, pr, tq[u]);
+          for (int c = 0; c < kCols; ++c) {
+            float pr = fast_exp2(fmaf(v[c], sl2, kterm + ct[c]));
+            const int q = q0 + c;
+            if (q < key || q >= p.N) pr = 0.f;
+            if (q == qlast) lastp = pr;
+            ts[c & 3] += pr;
+            tq[c & 3] = fmaf(pr, pr, tq[c & 3]);
           }
+          dsum += (double)((ts[0] + ts[1]) + (ts[2] + ts[3]));
+          dsq += (double)((tq[0] + tq[1]) + (tq[2] + tq[3]));
+        } else if (slope_on) {
+#pragma unroll
+          for (int c = 0; c < kCols; c += 4) {
+            const float4 tt4 = *reinterpret_cast<const float4*>(ct + c);
+            const float tt[4] = {tt4.x, tt4.y, tt4.z, tt4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float xx = fmaf(v[c + u], sl2, kterm + tt[u]);
+              const float pr = exp2_mixed(xx, u);
+              ts[u] += pr;
+              tq[u] = fmaf(pr, pr, tq[u]);
+            }
+          }
+          dsum += (double)((ts[0] + ts[1]) + (ts[2] + ts[3]));
+          dsq += (double)((tq[0] + tq[1]) + (tq[2] + tq[3]));
+        } else {
+          // packed pairs: FFMA2 for the logits, FADD2 / FFMA2 for the two sums
+          const uint64_t s2x = f2_pack(sl2, sl2);
+          uint64_t as = f2_pack(0.f, 0.f), aq = f2_pack(0.f, 0.f);
+          uint64_t bs = f2_pack(0.f, 0.f), bq = f2_pack(0.f, 0.f);
+#pragma unroll
+          for (int c = 0; c < kCols; c += 4) {
+            const float4 tt4 = *reinterpret_cast<const float4*>(ct + c);
+            const uint64_t p0 = f2_exp2(f2_fma(f2_pack(v[c], v[c + 1]), s2x, f2_pack(tt4.x, tt4.y)));
+            const uint64_t x1 = f2_fma(f2_pack(v[c + 2], v[c + 3]), s2x, f2_pack(tt4.z, tt4.w));
+            // all on MUFU: a quarter on the FMA pipe measured 1.6 % slower here
+            // (config 4), while it gains 5 % in the row pass
+            const uint64_t p1 = f2_exp2(x1);
+            as = f2_add(as, p0);
+            aq = f2_fma(p0, p0, aq);
+            bs = f2_add(bs, p1);
+            bq = f2_fma(p1, p1, bq);
+          }
+          float x0, x1, x2, x3, y0, y1, y2, y3;
+          f2_unpack(as, x0, x1);
+          f2_unpack(bs, x2, x3);
+          f2_unpack(aq, y0, y1);
+          f2_unpack(bq, y2, y3);
+          const float s1 = (x0 + x1) + (x2 + x3);
+          const float s2 = (y0 + y1) + (y2 + y3);
+          dsum += (double)(s1 * kfac);
+          dsq += (double)(s2 * (kfac * kfac));
         }
-        dsum += (double)((ts[0] + ts[1]) + (ts[2] + ts[3]));
-        dsq += (double)((tq[0] + tq[1]) + (tq[2] + tq[3]));
-      } else {
-        // packed pairs: FFMA2 for the logits, FADD2 / FFMA2 for the two sums
-        const uint64_t s2x = f2_pack(sl2, sl2);
-        uint64_t as = f2_pack(0.f, 0.f), aq = f2_pack(0.f, 0.f);
-        uint64_t bs = f2_pack(0.f, 0.f), bq = f2_pack(0.f, 0.f);
-#pragma unroll
-        for (int c = 0; c < kCols; c += 4) {
-          const float4 t = *reinterpret_cast<const float4*>(ct + c);
-          const uint64_t p0 = f2_exp2(f2_fma(f2_pack(v[c], v[c + 1]), s2x, f2_pack(t.x, t.y)));
-          const uint64_t x1 = f2_fma(f2_pack(v[c + 2], v[c + 3]), s2x, f2_pack(t.z, t.w));
-          // all on MUFU: a quarter on the FMA pipe measured 1.6 % slower here
-          // (config 4), while it gains 5 % in the row pass
-          const uint64_t p1 = f2_exp2(x1);
-          as = f2_add(as, p0);
-          aq = f2_fma(p0, p0, aq);
-          bs = f2_add(bs, p1);
-          bq = f2_fma(p1, p1, bq);
-        }
-        float x0, x1, x2, x3, y0, y1, y2, y3;
-        f2_unpack(as, x0, x1);
-        f2_unpack(bs, x2, x3);
-        f2_unpack(aq, y0, y1);
-        f2_unpack(bq, y2, y3);
-        const float s1 = (x0 + x1) + (x2 + x3);
-        const float s2 = (y0 + y1) + (y2 + y3);
-        dsum += (double)(s1 * kfac);
-        dsq += (double)(s2 * (kfac * kfac));
       }
-    }
-    // the last query row lies in the last (masked) tile; merge the groups
-    if (half > 0) { s_part[0][half][kl] = dsum; s_part[1][half][kl] = dsq; s_plast[half][kl] = lastp; }
-    EpiSync::sync();
-    if (half == 0) {
-#pragma unroll
-      for (int gq = 1; gq < kGroups; ++gq) {
-        dsum += s_part[0][gq][kl];
-        dsq += s_part[1][gq][kl];
-        lastp += s_plast[gq][kl];
-      }
-      if (key >= p.N) lastp = 0.f;
-      if (key < p.N) {
-        p.colsum[(size_t)g * p.N + key] = dsum;
-        p.colsq[(size_t)g * p.N + key] = dsq;
-        p.lastp[(size_t)g * p.N + key] = lastp;
-      }
-      s_lastp[kl] = lastp;
-    }
-    EpiSync::sync();
-    {
-      // last-row output partial of this key tile, sum_j lastp_j V_j, by all
-      // epilogue threads: 16-byte loads of 8 dims, every load in flight at
-      // once (a per-dimension loop here was a chain of ~30 L2/DRAM round
-      // trips at the end of every CTA); partials meet in the drained rings
-      static_assert(kTT * 128 / 8 == 8 * 32 * kEpiWarps, "16-byte loads per epilogue thread");
-      constexpr int RG = 32 * kEpiWarps / 16;  // row groups
-      const __nv_bfloat16* vt = p.v + ((size_t)g * p.ld + (size_t)kt * kTT) * 128;
-      const int nrow = min(kTT, p.N - kt * kTT);
-      const int c = et & 15, r0 = et >> 4;
-      uint4 raw[kTT / RG];
-#pragma unroll
-      for (int k = 0; k < kTT / RG; ++k) {
-        const int j = r0 + RG * k;
-        raw[k] = j < nrow ? ld_nc_v4(vt + (size_t)j * 128 + c * 8) : make_uint4(0u, 0u, 0u, 0u);
-      }
-      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int k = 0; k < kTT / RG; ++k) {
-        const int j = r0 + RG * k;
-        const float w = j < nrow ? s_lastp[j] : 0.f;
-        float f[8];
-        Elem<__nv_bfloat16>::unpack(raw[k], f);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] = fmaf(w, f[e], acc[e]);
-      }
-      float* red = reinterpret_cast<float*>(smem);  // [RG][128]; all TMA / MMA work is done
-#pragma unroll
-      for (int e = 0; e < 8; ++e) red[r0 * 128 + c * 8 + e] = acc[e];
+      // the last query row lies in the last (masked) tile; merge the groups
+      if (half > 0) { s_part[0][half][kl] = dsum; s_part[1][half][kl] = dsq; s_plast[half][kl] = lastp; }
       EpiSync::sync();
       if (half == 0) {
-        float o = 0.f;
 #pragma unroll
-        for (int r = 0; r < RG; ++r) o += red[r * 128 + et];
-        p.out_part[((size_t)g * ntiles + kt) * 128 + et] = o;
+        for (int gq = 1; gq < kGroups; ++gq) {
+          dsum += s_part[0][gq][kl];
+          dsq += s_part[1][gq][kl];
+          lastp += s_plast[gq][kl];
+        }
+        if (key >= p.N) lastp = 0.f;
+        if (key < p.N) {
+          p.colsum[(size_t)g * p.N + key] = dsum;
+          p.colsq[(size_t)g * p.N + key] = dsq;
+          p.lastp[(size_t)g * p.N + key] = lastp;
+        }
+        s_lastp[kl] = lastp;
+      }
+      EpiSync::sync();
+      {
+        // last-row output partial of this key tile, sum_j lastp_j V_j, by all
+        // epilogue threads: 16-byte loads of 8 dims, every load in flight at
+        // once (a per-dimension loop here was a chain of ~30 L2/DRAM round
+        // trips at the end of every CTA); partials meet in s_red
+        static_assert(kTT * 128 / 8 == 8 * 32 * kEpiWarps, "16-byte loads per epilogue thread");
+        constexpr int RG = 32 * kEpiWarps / 16;  // row groups
+        const __nv_bfloat16* vt = p.v + ((size_t)g * p.ld + (size_t)kt * kTT) * 128;
+        const int nrow = min(kTT, p.N - kt * kTT);
+        const int c = et & 15, r0 = et >> 4;
+        uint4 raw[kTT / RG];
+#pragma unroll
+        for (int k = 0; k < kTT / RG; ++k) {
+          const int jr = r0 + RG * k;
+          raw[k] = jr < nrow ? ld_nc_v4(vt + (size_t)jr * 128 + c * 8) : make_uint4(0u, 0u, 0u, 0u);
+        }
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int k = 0; k < kTT / RG; ++k) {
+          const int jr = r0 + RG * k;
+          const float w = jr < nrow ? s_lastp[jr] : 0.f;
+          float f[8];
+          Elem<__nv_bfloat16>::unpack(raw[k], f);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] = fmaf(w, f[e], acc[e]);
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s_red[r0 * 128 + c * 8 + e] = acc[e];
+        EpiSync::sync();
+        if (half == 0) {
+          float o = 0.f;
+#pragma unroll
+          for (int r = 0; r < RG; ++r) o += s_red[r * 128 + et];
+          p.out_part[((size_t)g * ntiles + kt) * 128 + et] = o;
+        }
+        EpiSync::sync();  // s_red / s_lastp / s_part are reused by the next item
       }
     }
   }
@@ -547,22 +572,21 @@ cudaError_t launch_tc_passes(const void* q, const void* k, const void* v, int B,
     cudaError_t r = cudaFuncSetAttribute(k1tc_rowlse, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kTcSmem);
     if (r == cudaSuccess)
-      r = cudaFuncSetAttribute(k1tc_colsum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
+      r = cudaFuncSetAttribute(k1tc_colsum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmemCol);
     return r;
   });
   if (e != cudaSuccess) return e;
   TcParams p{H, N, ld, cls, cls_ld, slope, sink, static_cast<const __nv_bfloat16*>(v), lse, colsum,
              colsq, lastp, out_part, (float)(1.0 / sqrt(128.0))};
-  const dim3 grid(tc_tiles(N), G);
-  const dim3 pairs((tc_tiles(N) + 1) / 2, G);  // query tiles x and ntiles-1-x share a CTA
+  const dim3 pairs((tc_tiles(N) + 1) / 2, G);  // tiles x and ntiles-1-x share a CTA
   k1tc_rowlse<<<pairs, kTcThreads, kTcSmem, st>>>(p, tmQ, tmK);
   if ((e = cudaGetLastError())) return e;
   {  // programmatic dependent launch: setup, K/Q loads and the first MMAs
      // overlap the row pass's tail
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = grid;
+    cfg.gridDim = pairs;  // key tiles x and ntiles-1-x share a CTA
     cfg.blockDim = dim3(kTcThreads);
-    cfg.dynamicSmemBytes = kTcSmem;
+    cfg.dynamicSmemBytes = kTcSmemCol;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
