@@ -1011,9 +1011,12 @@ def bench_reference(args):
         for b, h in mine:
             groups.setdefault(b, []).append(h)
         jobs.append((w.seed, sorted(groups.items()), T, w.B, w.H, w.N, w.D, kind))
+    # one warm-up session primes the worker pool and its inputs; the CPU
+    # path has nothing else to warm, and a full session takes ~10 s
+    warm = min(args.warmup, 1)
     ctx = mp.get_context("fork")
     with ctx.Pool(workers) as pool:
-        for _ in range(args.warmup):
+        for _ in range(warm):
             pool.map(_cpu_job, jobs)
         times = []
         for _ in range(args.steps):
@@ -1026,7 +1029,7 @@ def bench_reference(args):
         "impl": "reference",
         "metric": "decode tok/s with adaptive KV at fixed T (session incl. profiling)",
         "value": value, "unit": "tok/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+        "steps": args.steps, "warmup": warm, "ms_per_step": step_s * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (same seeded workload as the GPU arm)",
         "config": {"workload": f"c1 Llama-7B-shape layer: B={w.B} H={w.H} d={w.d} N={w.N} "

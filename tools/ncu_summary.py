@@ -86,8 +86,13 @@ def report(path, tag):
         name = d.get("Kernel Name", "?").split("(")[0].replace("void ", "")
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         tot = sum(float(d[k]) * scale.get(u[k], 1) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-        data[name] = {"dram_bytes_per_launch": tot, "source": f"profiles/{tag}_{base}.md",
-                      "duration_us": float(d["gpu__time_duration.sum"])}
+        entry = {"dram_bytes_per_launch": tot, "source": f"profiles/{tag}_{base}.md",
+                 "duration_us": float(d["gpu__time_duration.sum"])}
+        # keyed by kernel and by kernel@capture (several captures of one
+        # kernel, e.g. K3 in the headline and in the FREQUENT-heavy regime)
+        data[f"{name}@{base}"] = entry
+        if base in ("k3_full", "k1k2_full", "k2_full", "diag_full") or name not in data:
+            data[name] = entry
     with open(tj, "w") as f:
         json.dump(data, f, indent=1, sort_keys=True)
 

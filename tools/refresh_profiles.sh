@@ -4,7 +4,7 @@
 #   launch list of the bench command (cold-cache, serialised: compare shares)
 #   --set full of K1 (both passes + policy) and K2 at config 1 and K1 at config 4,
 #   K3 mid-session at config 1, the diagnostics kernel.
-# Then locally: python tools/ncu_summary.py r1 gpurun_out/launches.csv gpurun_out/*.ncu-rep
+# Then locally: python tools/ncu_summary.py r2 gpurun_out/launches.csv gpurun_out/*.ncu-rep
 set -u
 OUT=gpurun_out
 mkdir -p $OUT
@@ -17,6 +17,8 @@ python tools/profile_targets.py k3 > $OUT/pre_k3.log || exit 1
 $FULL -k regex:'k1tc_|k1_policy' -c 3 -o $OUT/k1k2_full -f python tools/profile_targets.py k3 > $OUT/ncu_k1.log 2>&1
 $FULL -k regex:'k2_compact' -c 1 -o $OUT/k2_full -f python tools/profile_targets.py k3 > $OUT/ncu_k2.log 2>&1
 $FULL -k regex:'k3_decode' -s 200 -c 1 -o $OUT/k3_full -f python tools/profile_targets.py k3 > $OUT/ncu_k3.log 2>&1
+python tools/profile_targets.py k3f > $OUT/pre_k3f.log || exit 1
+$FULL -k regex:'k3_decode' -s 200 -c 1 -o $OUT/k3f_full -f python tools/profile_targets.py k3f > $OUT/ncu_k3f.log 2>&1
 python tools/profile_targets.py diag > $OUT/pre_diag.log || exit 1
 $FULL -k regex:'decode_recovery' -s 200 -c 1 -o $OUT/diag_full -f python tools/profile_targets.py diag > $OUT/ncu_diag.log 2>&1
 python tools/k1_timing.py c4 > $OUT/pre_c4.log || exit 1
