@@ -6,6 +6,7 @@ short session produce identical tokens).
 
     python tools/run_llama.py c2 [--layers L] [--batch B] [--prompt N] [--decode D] [--T 0.95]
     torchrun --nproc-per-node P tools/run_llama.py c2 --mode gather|tp|dp
+    python tools/run_llama.py c3 --mode tp --gpus 8      # spawns the 8 ranks itself
 
 Config 2 = Llama-7B shape (32 layers, d_model 4096, 32 heads, SwiGLU 11008,
 vocab 32000), batch 16, prompt 2048, greedy decode 512; config 3 = Llama-65B
@@ -41,6 +42,13 @@ def prompt_ids(B, N, vocab, seed):
     return ids
 
 
+def _spawned(index, world, port, argv):
+    os.environ.update({"RANK": str(index), "LOCAL_RANK": str(index), "WORLD_SIZE": str(world),
+                       "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    sys.argv = argv
+    main()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("config", choices=sorted(PRESETS))
@@ -56,7 +64,19 @@ def main():
                          "collectives (per-GPU compute of a multi-GPU config on one GPU)")
     ap.add_argument("--diagnostics", action="store_true",
                     help="per-step recovery vs uncompressed attention (shadow keys)")
+    ap.add_argument("--gpus", type=int, default=1,
+                    help="without torchrun: spawn one process per GPU (NCCL), like bench.py")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        import socket
+
+        import torch.multiprocessing as tmp
+
+        with socket.socket() as s_:
+            s_.bind(("127.0.0.1", 0))
+            port = s_.getsockname()[1]
+        tmp.spawn(_spawned, args=(args.gpus, port, list(sys.argv)), nprocs=args.gpus, join=True)
+        return
     cfg, B, N, D = PRESETS[args.config]
     if args.layers:
         cfg = type(cfg)(**{**cfg.__dict__, "n_layers": args.layers})
