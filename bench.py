@@ -204,7 +204,8 @@ class Ranks:
     no data-path collective (heads / batch rows are independent,
     engine.py:182-199, 236-259, 310-349)."""
 
-    def __init__(self):
+    def __init__(self, cpu: bool = False):
+        """cpu=True (tests only): gloo between CPU processes, no device."""
         import torch
 
         self.rank = int(os.environ.get("RANK", "0"))
@@ -213,21 +214,23 @@ class Ranks:
         # AKV_BENCH_ONE_DEVICE=1 (code-path check only): every rank on cuda:0
         # over gloo, so the multi-rank path can be exercised on a one-GPU
         # box; its numbers are not measurements
-        self.one_dev = os.environ.get("AKV_BENCH_ONE_DEVICE") == "1"
+        self.one_dev = cpu or os.environ.get("AKV_BENCH_ONE_DEVICE") == "1"
         if self.one_dev:
             self.local = 0
         self.dist = None
         if self.world > 1:
             import torch.distributed as dist
 
-            torch.cuda.set_device(self.local)
+            if not cpu:
+                torch.cuda.set_device(self.local)
             if self.one_dev:
                 dist.init_process_group("gloo")
             else:
                 dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
             self.dist = dist
-        self.dev = torch.device("cuda", self.local)
-        torch.cuda.set_device(self.dev)
+        self.dev = torch.device("cpu") if cpu else torch.device("cuda", self.local)
+        if not cpu:
+            torch.cuda.set_device(self.dev)
 
     def barrier(self):
         if self.dist is not None:
@@ -547,7 +550,7 @@ def bench_extras_multi(T, R, peaks, args, rank0_line):
 
     import torch
 
-    from paper_2310_01801_b200.parallel import (assignment_loads, head_shard, lpt_assignment)
+    from paper_2310_01801_b200.parallel import head_shard
     from paper_2310_01801_b200.workloads import config1, config4
 
     out = {}
@@ -568,14 +571,7 @@ def bench_extras_multi(T, R, peaks, args, rank0_line):
     r = _extra_session(w4.heads(sh.h0, sh.h1), T, R, peaks)
     enc, decm = R.max(r["enc_ms"], r["dec_ms"])
     ranks = R.gather({k: r[k] for k in ("enc_ms", "dec_ms", "gbs", "frac", "retained", "costs")})
-    # decode cost per head (kept + D live rows), global (b, h) order
-    costs = np.zeros((w4.B, w4.H), np.int64)
-    for rr, part in enumerate(ranks):
-        s_ = head_shard(w4.B, w4.H, R.world, rr)
-        costs[:, s_.h0:s_.h1] = np.asarray(part["costs"]).reshape(w4.B, s_.h1 - s_.h0)
-    flat = costs.reshape(-1).tolist()
-    contig = [sum(part["costs"]) for part in ranks]
-    lpt = assignment_loads(flat, lpt_assignment(flat, R.world))
+    balance = shard_balance(w4.B, w4.H, [part["costs"] for part in ranks])
     N, D = w4.N, w4.D
     out["c4_head_sharded"] = {
         "workload": f"long context: B={w4.B} H={w4.H} d={w4.d} N={N} D={D} bf16, T={T:g}; "
@@ -586,9 +582,7 @@ def bench_extras_multi(T, R, peaks, args, rank0_line):
         "per_rank": [{"rank": i, "decode_us_per_step": p["dec_ms"] * 1e3 / D,
                       "k3_gbs": p["gbs"], "k3_frac_of_hbm_peak": p["frac"]}
                      for i, p in enumerate(ranks)],
-        "balance": {"contiguous_max_over_mean": max(contig) / (sum(contig) / len(contig)),
-                    "lpt_max_over_mean": max(lpt) / (sum(lpt) / len(lpt)),
-                    "basis": "decode live rows per rank (kept + D per head) after profiling"},
+        "balance": balance,
         "pruned_ratio_end": 1.0 - sum(p["retained"] for p in ranks) / float(w4.B * w4.H * (N + D)),
     }
 
@@ -623,6 +617,26 @@ def bench_extras_multi(T, R, peaks, args, rank0_line):
             out["c2_gather"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     dog.cancel()
     return out
+
+
+def shard_balance(B, H, rank_costs):
+    """Load balance of a head sharding after profiling: rank r's decode costs
+    (kept + D live rows per head, its heads [h0, h1) of every batch row, in
+    (b, h) order) -> max/mean load of the contiguous split the bench ran and
+    of parallel.lpt_assignment over the same costs."""
+    from paper_2310_01801_b200.parallel import assignment_loads, head_shard, lpt_assignment
+
+    world = len(rank_costs)
+    costs = np.zeros((B, H), np.int64)
+    for rr, part in enumerate(rank_costs):
+        s_ = head_shard(B, H, world, rr)
+        costs[:, s_.h0:s_.h1] = np.asarray(part).reshape(B, s_.h1 - s_.h0)
+    flat = costs.reshape(-1).tolist()
+    contig = [int(sum(part)) for part in rank_costs]
+    lpt = assignment_loads(flat, lpt_assignment(flat, world))
+    return {"contiguous_max_over_mean": max(contig) / (sum(contig) / len(contig)),
+            "lpt_max_over_mean": max(lpt) / (sum(lpt) / len(lpt)),
+            "basis": "decode live rows per rank (kept + D per head) after profiling"}
 
 
 def _c2_decode(T, dev, peaks, R=None):

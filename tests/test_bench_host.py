@@ -123,3 +123,50 @@ def test_reference_leg_matches_the_oracle_port_on_a_small_session():
         for t in range(w.D):
             O.decode_head(st, q[N + t], k[N + t], v[N + t], N + t, cls, N)
         assert list(np.sort(st.positions)) == cache.heads[(0, i)].positions
+
+
+def _ranks_worker(rank, world, port, q):
+    import os
+
+    os.environ.update({"RANK": str(rank), "WORLD_SIZE": str(world), "LOCAL_RANK": str(rank),
+                       "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    import bench
+
+    R = bench.Ranks(cpu=True)
+    mx = R.max(float(rank), 10.0 - rank)
+    got = R.gather({"rank": rank})
+    # each rank's decode costs of its head shard of a B=2 x H=4 workload
+    from paper_2310_01801_b200.parallel import head_shard
+
+    sh = head_shard(2, 4, world, rank)
+    costs = [100 * (b + 1) + h for b in range(2) for h in range(sh.h0, sh.h1)]
+    bal = bench.shard_balance(2, 4, R.gather(costs))
+    R.barrier()
+    q.put((rank, mx, got, bal))
+    R.dist.destroy_process_group()
+
+
+def test_bench_ranks_and_balance_under_gloo():
+    """bench.py's multi-rank plumbing (max over ranks, gather, the head-shard
+    balance report) with world size 2 over gloo on CPU."""
+    import multiprocessing as mp
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ranks_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in procs:
+        p_.start()
+    out = sorted(q.get(timeout=120) for _ in procs)
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    for rank, mx, got, bal in out:
+        assert mx == [1.0, 10.0]
+        assert got == [{"rank": 0}, {"rank": 1}]
+        # heads 0-1 on rank 0: 100+101+200+201 = 602; heads 2-3: 102+103+202+203 = 610
+        assert abs(bal["contiguous_max_over_mean"] - 610 / 606) < 1e-12
+        assert bal["lpt_max_over_mean"] <= bal["contiguous_max_over_mean"] + 1e-12
