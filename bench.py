@@ -554,7 +554,7 @@ def bench_extras_multi(T, R, peaks, args, rank0_line):
     from paper_2310_01801_b200.workloads import config1, config4
 
     out = {}
-    limit = float(os.environ.get("AKV_BENCH_EXTRAS_TIMEOUT", "600"))
+    limit = float(os.environ.get("AKV_BENCH_EXTRAS_TIMEOUT", "240"))
 
     def _expire():
         if R.rank == 0:
