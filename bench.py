@@ -156,7 +156,8 @@ def run_session(w, T, qd, kd, vd, cd, slopes, sinks, decode_inputs, ev=None, rec
     when ``record``, the live slot counts before every decode step."""
     import torch
 
-    from paper_2310_01801_b200 import ProfilerConfig, decode_step_tensors, encode_prompt_tensors
+    from paper_2310_01801_b200 import (ProfilerConfig, decode_step_tensors, decode_steps_tensors,
+                                       encode_prompt_tensors)
 
     cfg = ProfilerConfig(recovery_threshold=T)
     pool = arena_pool(w, qd.device)
@@ -169,10 +170,15 @@ def run_session(w, T, qd, kd, vd, cd, slopes, sinks, decode_inputs, ev=None, rec
         ev[1].record()
     lives = []
     dq, dk, dv, dc = decode_inputs
-    for t in range(w.D):
-        if record:
+    if record:
+        for t in range(w.D):
             lives.append(cache.live.cpu().numpy().copy())
-        decode_step_tensors(cache, dq[t], dk[t], dv[t], dc[t], chained=True)
+            decode_step_tensors(cache, dq[t], dk[t], dv[t], dc[t], chained=True)
+    else:
+        # the D teacher-forced steps in one call (the step loop in C++)
+        N = w.N
+        decode_steps_tensors(cache, qd[:, :, N:N + w.D], kd[:, :, N:N + w.D], vd[:, :, N:N + w.D],
+                             dc.steps, chained=True)
     if ev is not None:
         ev[2].record()
     if record:
@@ -257,9 +263,16 @@ class Ranks:
         return out
 
 
+class _Classes(list):
+    """Per-step class columns [B] (a list, for step-by-step calls) that also
+    carries them step-major, ``steps`` [D, B] (for decode_steps_tensors)."""
+
+
 def _dec_inputs(qd, kd, vd, cd, N, D):
+    cls = _Classes(cd[:, N + t].contiguous() for t in range(D))
+    cls.steps = cd[:, N:N + D].t().contiguous()
     return ([qd[:, :, N + t] for t in range(D)], [kd[:, :, N + t] for t in range(D)],
-            [vd[:, :, N + t] for t in range(D)], [cd[:, N + t].contiguous() for t in range(D)])
+            [vd[:, :, N + t] for t in range(D)], cls)
 
 
 def _policy_counts(res):
@@ -731,7 +744,7 @@ def bench_e2e(w, T, args, qh, kh, vh, clsh, slopes, sinks, dev, R):
     outputs return in 128-step chunks while later steps run."""
     import torch
 
-    from paper_2310_01801_b200 import ProfilerConfig, decode_step_tensors, encode_prompt_tensors
+    from paper_2310_01801_b200 import ProfilerConfig, decode_steps_tensors, encode_prompt_tensors
 
     N, D, B, H, d = w.N, w.D, w.B, w.H, w.d
     dt = torch.bfloat16 if w.dtype == "bf16" else torch.float32
@@ -759,16 +772,19 @@ def bench_e2e(w, T, args, qh, kh, vh, clsh, slopes, sinks, dev, R):
     pc = [torch.empty(B, N, dtype=torch.uint8, device=dev) for _ in range(2)]
     rows = [torch.empty(D, row_bytes, dtype=torch.uint8, device=dev) for _ in range(2)]
 
-    def _views(x):
-        return (x[0:rb].view(dt).view(B, H, d), x[rb:2 * rb].view(dt).view(B, H, d),
-                x[2 * rb:3 * rb].view(dt).view(B, H, d), x[3 * rb:3 * rb + B])
-
-    # tensor views built once: the per-step host work is only the launch
     # two output buffers: a session's last output chunk drains to the host
     # while the next session already runs
     dout = [torch.empty(D, B, H, d, dtype=torch.float32, device=dev) for _ in range(2)]
-    step_views = [[_views(rows[s][t]) for t in range(D)] for s in range(2)]
-    out_views = [[dout[s][t] for t in range(D)] for s in range(2)]
+
+    def _seq(buf):
+        """step-sliceable views of a session's packed rows: q / k / v
+        [B, H, D, d] (step t = [:, :, t]) and the classes [D, B]"""
+        el = buf.view(dt)                       # [D, row_bytes / es]
+        n = rb // es
+        part = lambda i: el[:, i * n:(i + 1) * n].view(D, B, H, d).permute(1, 2, 0, 3)  # noqa: E731
+        return part(0), part(1), part(2), buf[:, 3 * rb:3 * rb + B]
+
+    seq_views = [_seq(rows[s]) for s in range(2)]
     ev = lambda: torch.cuda.Event()
     ready, free = [ev(), ev()], [ev(), ev()]
     CH = 128
@@ -795,17 +811,18 @@ def bench_e2e(w, T, args, qh, kh, vh, clsh, slopes, sinks, dev, R):
                                          max_new_tokens=D, slopes=slopes, sinks=sinks, pool=pool)
         if prefetch_next:
             upload(slot ^ 1)
-        sv = step_views[slot]
-        for t in range(D):
-            q, k, v, c = sv[t]
-            decode_step_tensors(cache, q, k, v, c, out=out_views[slot][t], chained=True)
-            if (t + 1) % CH == 0 or t + 1 == D:
-                c0 = (t // CH) * CH
-                e = chunk_done[t // CH]
-                e.record(main)
-                with torch.cuda.stream(cs):
-                    cs.wait_event(e)
-                    hout[c0:t + 1].copy_(dout[slot][c0:t + 1], non_blocking=True)
+        qs, ks, vs, cls = seq_views[slot]
+        for c0 in range(0, D, CH):
+            c1 = min(D, c0 + CH)
+            # a chunk of teacher-forced steps in one call; its outputs then
+            # drain to the host on the copy stream while later steps run
+            decode_steps_tensors(cache, qs[:, :, c0:c1], ks[:, :, c0:c1], vs[:, :, c0:c1],
+                                 cls[c0:c1], out=dout[slot][c0:c1], chained=True)
+            e = chunk_done[c0 // CH]
+            e.record(main)
+            with torch.cuda.stream(cs):
+                cs.wait_event(e)
+                hout[c0:c1].copy_(dout[slot][c0:c1], non_blocking=True)
         free[slot].record(main)
         with torch.cuda.stream(cs):
             out_free[slot].record(cs)

@@ -230,6 +230,18 @@ typedef struct akv_decode_args {
 
 size_t akv_decode_workspace_size(int32_t B, int32_t H, int32_t d, int32_t max_cap, int64_t total_slots);
 int akv_decode_step(const akv_decode_args* a, void* stream);
+/* n_steps consecutive teacher-forced decode steps in one call (engine.py:283-371
+ * applied n times with known tokens: trace replay, benchmarks, prompt-extension
+ * checks): step s inserts position pos + s, reads q/k/v at *_dev + s*step_stride
+ * elements and classes at new_cls_dev + s*cls_step_stride; live counts
+ * alternate between live_in_dev and live_out_dev (after the call they are in
+ * live_out_dev for odd n_steps, live_in_dev for even); step s writes its output
+ * to out_steps + s*out_step_stride (fp32), or to out_dev when out_steps is
+ * NULL.  `flags` apply to step 0; later steps are chained.  pos_dev must be
+ * NULL. */
+int akv_decode_steps(const akv_decode_args* a, int32_t n_steps, int64_t step_stride,
+                     int64_t cls_step_stride, float* out_steps, int64_t out_step_stride,
+                     void* stream);
 /* Zero the decode workspace counters (call once after allocating it). */
 int akv_decode_workspace_init(void* workspace_dev, size_t workspace_bytes, int32_t B, int32_t H,
                               int32_t d, int32_t max_cap, int64_t total_slots, void* stream);

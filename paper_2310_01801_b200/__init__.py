@@ -13,6 +13,7 @@ from .attention import (AttentionError, AttentionMap, causal_attention, softmax_
 from .engine import (ArenaPool, CompressedCache, EngineError, GenerationConfig, GenerationResult,
                      HeadCacheState,
                      GreedyArgmax, Nucleus, ProfileResult, StepRecord, decode_step_tensors,
+                     decode_steps_tensors,
                      encode_prompt, encode_prompt_tensors, generate, generate_fixed_baseline,
                      generate_step, grow_cache, records_to_ndjson, reference_generate)
 from .policies import (DEFAULT_FEASIBLE_ORDER, DEFAULT_RATIO, CompressionPolicy, PolicyAtom,

@@ -104,7 +104,7 @@ class DiagArgs(C.Structure):
 EXPORTS = (
     "akv_profile_workspace_size", "akv_profile", "akv_compact", "akv_plan_segments",
     "akv_plan_segments_pool",
-    "akv_decode_workspace_size", "akv_decode_step", "akv_decode_workspace_init",
+    "akv_decode_workspace_size", "akv_decode_step", "akv_decode_steps", "akv_decode_workspace_init",
     "akv_decode_recovery", "akv_decode_recovery_workspace_size",
     "akv_decode_recovery_workspace_init",
     "akv_softmax_rows_f64", "akv_causal_attention_f64", "akv_keep_mask", "akv_map_recovery_f64",
@@ -134,6 +134,8 @@ def _load():
     lib.akv_decode_workspace_size.argtypes = [i32, i32, i32, i32, i64]
     lib.akv_decode_step.restype = C.c_int
     lib.akv_decode_step.argtypes = [C.POINTER(DecodeArgs), P]
+    lib.akv_decode_steps.restype = C.c_int
+    lib.akv_decode_steps.argtypes = [C.POINTER(DecodeArgs), i32, i64, i64, P, i64, P]
     lib.akv_decode_workspace_init.restype = C.c_int
     lib.akv_decode_workspace_init.argtypes = [P, sz, i32, i32, i32, i32, i64, P]
     lib.akv_softmax_rows_f64.argtypes = [i32, i32, P, P, P, P]

@@ -1589,3 +1589,37 @@ extern "C" int akv_decode_step(const akv_decode_args* a, void* stream) {
   if (e != cudaSuccess) return set_error(AKV_ERR_CUDA, "akv_decode_step: %s", cudaGetErrorString(e));
   return AKV_OK;
 }
+
+// n consecutive teacher-forced decode steps in one call (the host loop in
+// C++: a launch costs ~2-3 us of host time instead of a Python call's
+// ~10-13 us, which bounds small batches).  Step s inserts position pos + s,
+// reads q/k/v at q_dev/k_dev/v_dev + s*step_stride elements and the classes
+// at new_cls_dev + s*cls_step_stride; the live counts alternate between
+// live_in_dev and live_out_dev (after the call they are in live_out_dev for
+// odd n, live_in_dev for even n); step s writes its output to
+// out_steps + s*out_step_stride, or to out_dev when out_steps is NULL.
+// `flags` apply to step 0; later steps are chained (their predecessor is the
+// previous step and their inputs were resident before the call).
+extern "C" int akv_decode_steps(const akv_decode_args* a, int32_t n_steps, int64_t step_stride,
+                                int64_t cls_step_stride, float* out_steps, int64_t out_step_stride,
+                                void* stream) {
+  if (!a) return set_error(AKV_ERR_INVALID, "akv_decode_steps: null args");
+  if (n_steps < 0) return set_error(AKV_ERR_INVALID, "akv_decode_steps: n_steps < 0");
+  if (a->pos_dev) return set_error(AKV_ERR_INVALID, "akv_decode_steps: needs host positions (pos_dev is set)");
+  const size_t es = a->dtype == AKV_DTYPE_BF16 ? 2 : 4;
+  akv_decode_args s = *a;
+  for (int i = 0; i < n_steps; ++i) {
+    s.pos = a->pos + i;
+    s.q_dev = static_cast<const char*>(a->q_dev) + (int64_t)i * step_stride * (int64_t)es;
+    s.k_dev = static_cast<const char*>(a->k_dev) + (int64_t)i * step_stride * (int64_t)es;
+    s.v_dev = static_cast<const char*>(a->v_dev) + (int64_t)i * step_stride * (int64_t)es;
+    s.new_cls_dev = a->new_cls_dev + (int64_t)i * cls_step_stride;
+    s.live_in_dev = (i & 1) ? a->live_out_dev : a->live_in_dev;
+    s.live_out_dev = (i & 1) ? const_cast<int32_t*>(a->live_in_dev) : a->live_out_dev;
+    s.out_dev = out_steps ? out_steps + (int64_t)i * out_step_stride : a->out_dev;
+    s.flags = i == 0 ? a->flags : (a->flags | AKV_DECODE_CHAINED);
+    const int rc = akv_decode_step(&s, stream);
+    if (rc != AKV_OK) return rc;
+  }
+  return AKV_OK;
+}

@@ -661,6 +661,57 @@ def decode_step_tensors(cache: CompressedCache, q, k, v, new_classes, out=None, 
     return dst
 
 
+def decode_steps_tensors(cache: CompressedCache, q, k, v, new_classes, out=None, *,
+                         chained: bool = False) -> torch.Tensor:
+    """n teacher-forced decode steps in one library call (the step loop runs
+    in C++, akv_decode_steps): q, k, v are [B, H, n, >=d] CUDA tensors whose
+    [:, :, t] slices are step t's new-token rows (the same strides for all
+    three), ``new_classes`` is uint8 [n, B] (contiguous rows: step t's
+    classes).  Returns the fp32 outputs: ``out`` [n, B, H, d] if given
+    (contiguous), else the last step's output in the cache's pending-output
+    buffer.  Same results as n calls of decode_step_tensors; ``chained``
+    applies to the first step (later steps are chained by construction).
+    Diagnostics-mode caches step one at a time (the recovery kernel runs
+    between steps)."""
+    n = int(q.shape[2])
+    if new_classes.dim() != 2 or tuple(new_classes.shape) != (n, cache.B) or \
+            (cache.B > 1 and new_classes.stride(1) != 1) or new_classes.dtype != torch.uint8:
+        raise EngineError(f"new_classes must be a contiguous uint8 [{n}, {cache.B}] tensor")
+    if k.shape[2] != n or v.shape[2] != n or k.stride() != q.stride() or v.stride() != q.stride():
+        raise EngineError("q, k and v must have the same shape and strides")
+    if out is not None and (tuple(out.shape) != (n, cache.B, cache.H, cache.d) or
+                            not out.is_contiguous() or out.dtype != torch.float32):
+        raise EngineError(f"out must be a contiguous float32 [{n}, {cache.B}, {cache.H}, {cache.d}]")
+    if cache.track_recovery:
+        for t in range(n):
+            decode_step_tensors(cache, q[:, :, t], k[:, :, t], v[:, :, t], new_classes[t],
+                                None if out is None else out[t], chained=chained)
+        return cache.out if out is None else out
+    if n == 0:
+        return cache.out if out is None else out
+    if cache.seq_len + n - cache.prompt_len > cache.capacity_steps:
+        raise EngineError(
+            f"cache capacity of {cache.capacity_steps} decode steps exhausted; "
+            "encode with a larger max_new_tokens")
+    a = cache._dargs
+    a.pos = cache.seq_len
+    a.q_dev, a.k_dev, a.v_dev = _ptr(q), _ptr(k), _ptr(v)
+    a.bh_stride = q.stride(1)
+    a.new_cls_dev = _ptr(new_classes)
+    a.live_in_dev = _ptr(cache.live_buf[cache._parity])
+    a.live_out_dev = _ptr(cache.live_buf[cache._parity ^ 1])
+    a.out_dev = _ptr(cache.out)
+    a.pos_dev = None
+    a.flags = _lib.DECODE_CHAINED if chained else 0
+    check(lib.akv_decode_steps(C.byref(a), n, q.stride(2), new_classes.stride(0),
+                               _ptr(out), 0 if out is None else out[0].numel(), _stream()),
+          EngineError)
+    cache._parity ^= n & 1
+    cache.seq_len += n
+    cache._latest_out = cache.out if out is None else out[n - 1]
+    return cache.out if out is None else out
+
+
 def decode_step_launch(cache: CompressedCache, q, k, v, new_classes, out, parity: int, pos_dev):
     """Launch one decode step whose insert position is read from the device
     (int32 ``pos_dev``) and whose live-count buffers are those of ``parity``,

@@ -432,7 +432,7 @@ def replay_tensors(trace: AttentionTrace, prompt_len: int, profiler_cfg=None, fi
     [steps, 1, G, d] fp32)."""
     import torch
 
-    from .engine import decode_step_tensors, encode_prompt_tensors
+    from .engine import decode_steps_tensors, encode_prompt_tensors
 
     q, k, v, cls = trace_tensors(trace, dtype)
     T = q.shape[2]
@@ -444,9 +444,8 @@ def replay_tensors(trace: AttentionTrace, prompt_len: int, profiler_cfg=None, fi
                                        diagnostics=diagnostics)
     outs = torch.empty(max(steps, 0), 1, q.shape[1], q.shape[3], dtype=torch.float32,
                        device=q.device)
-    new_cls = [cls[:, prompt_len + t].contiguous() for t in range(steps)]
-    for t in range(steps):
-        pos = prompt_len + t
-        decode_step_tensors(cache, q[:, :, pos], k[:, :, pos], v[:, :, pos], new_cls[t],
-                            out=outs[t], chained=True)
+    if steps > 0:   # the recorded positions, teacher-forced, in one library call
+        decode_steps_tensors(cache, q[:, :, prompt_len:], k[:, :, prompt_len:],
+                             v[:, :, prompt_len:], cls[:, prompt_len:].t().contiguous(),
+                             out=outs, chained=True)
     return res, cache, outs

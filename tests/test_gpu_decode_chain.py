@@ -119,3 +119,44 @@ def test_more_than_2048_heads_per_call():
                 np.testing.assert_array_equal(k[si][g], np.sort(st.positions),
                                               err_msg=f"head {g} step {t}")
                 si += 1
+
+
+@pytest.mark.parametrize("d,dtype", [(128, torch.bfloat16), (64, torch.float32)])
+def test_decode_steps_call_matches_step_by_step(d, dtype):
+    """akv_decode_steps (the step loop in C++, decode_steps_tensors) gives
+    bit-identical outputs, live counts and kept sets to one call per step."""
+    from paper_2310_01801_b200 import decode_steps_tensors
+
+    w = _workload(2, 6, 300, 40, d, seed=21)
+    qd, kd, vd, cd = _inputs(w)
+    qd, kd, vd = qd.to(dtype), kd.to(dtype), vd.to(dtype)
+    dev = qd.device
+    sl = torch.tensor(w.slopes, dtype=torch.float32, device=dev)
+    sk = torch.tensor(w.sinks, dtype=torch.float32, device=dev)
+    N, D = w.N, w.D
+    runs = []
+    for mode in ("steps", "single"):
+        res, c = encode_prompt_tensors(qd, kd, vd, cd, ProfilerConfig(recovery_threshold=0.98),
+                                       prompt_len=N, max_new_tokens=D, slopes=sl, sinks=sk)
+        outs = torch.empty(D, 2, w.H, d, dtype=torch.float32, device=dev)
+        if mode == "steps":   # two calls: 17 + 23 steps
+            cls = cd[:, N:].t().contiguous()
+            decode_steps_tensors(c, qd[:, :, N:N + 17], kd[:, :, N:N + 17], vd[:, :, N:N + 17],
+                                 cls[:17], out=outs[:17], chained=True)
+            decode_steps_tensors(c, qd[:, :, N + 17:], kd[:, :, N + 17:], vd[:, :, N + 17:],
+                                 cls[17:], out=outs[17:], chained=True)
+        else:
+            for t in range(D):
+                decode_step_tensors(c, qd[:, :, N + t], kd[:, :, N + t], vd[:, :, N + t],
+                                    cd[:, N + t].contiguous(), out=outs[t], chained=True)
+        torch.cuda.synchronize()
+        c.check()
+        runs.append((res.choice.copy(), outs.cpu().numpy(), c.live.cpu().numpy(),
+                     c.retained_positions(), c.seq_len))
+    a, b = runs
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[1], b[1])
+    np.testing.assert_array_equal(a[2], b[2])
+    assert a[4] == b[4] == N + D
+    for x, y in zip(a[3], b[3]):
+        np.testing.assert_array_equal(x, y)
