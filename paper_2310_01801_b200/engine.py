@@ -623,6 +623,21 @@ def _decode_args(cache: CompressedCache, dt: int) -> DecodeArgs:
     return a
 
 
+def _check_rows(cache: CompressedCache, q, k, v, step_dim: bool):
+    """The kernels read head g = b*H + h of q / k / v at g * q.stride(1)
+    elements (d contiguous values; k and v with q's strides)."""
+    nd = 4 if step_dim else 3
+    for name, x in (("q", q), ("k", k), ("v", v)):
+        if (x.dim() != nd or not x.is_cuda or x.dtype != cache.dtype or
+                tuple(x.shape[:2]) != (cache.B, cache.H) or x.shape[-1] < cache.d or
+                x.stride(-1) != 1 or (cache.B > 1 and x.stride(0) != cache.H * x.stride(1)) or
+                x.stride()[1:] != q.stride()[1:]):
+            raise EngineError(
+                f"{name} must be a CUDA {cache.dtype} tensor [B={cache.B}, H={cache.H}"
+                f"{', steps' if step_dim else ''}, >=d={cache.d}] with contiguous rows, batch "
+                "stride H x head stride, and the same strides as q")
+
+
 def decode_step_tensors(cache: CompressedCache, q, k, v, new_classes, out=None, *,
                         chained: bool = False) -> torch.Tensor:
     """One decode step for every head (Alg. 2 inner loop, engine.py:303-350):
@@ -640,6 +655,7 @@ def decode_step_tensors(cache: CompressedCache, q, k, v, new_classes, out=None, 
         raise EngineError(
             f"cache capacity of {cache.capacity_steps} decode steps exhausted; "
             "encode with a larger max_new_tokens")
+    _check_rows(cache, q, k, v, step_dim=False)
     a = cache._dargs
     a.pos = cache.seq_len
     a.q_dev, a.k_dev, a.v_dev = _ptr(q), _ptr(k), _ptr(v)
@@ -677,8 +693,9 @@ def decode_steps_tensors(cache: CompressedCache, q, k, v, new_classes, out=None,
     if new_classes.dim() != 2 or tuple(new_classes.shape) != (n, cache.B) or \
             (cache.B > 1 and new_classes.stride(1) != 1) or new_classes.dtype != torch.uint8:
         raise EngineError(f"new_classes must be a contiguous uint8 [{n}, {cache.B}] tensor")
-    if k.shape[2] != n or v.shape[2] != n or k.stride() != q.stride() or v.stride() != q.stride():
-        raise EngineError("q, k and v must have the same shape and strides")
+    if k.shape[2] != n or v.shape[2] != n:
+        raise EngineError("q, k and v must have the same number of steps")
+    _check_rows(cache, q, k, v, step_dim=True)
     if out is not None and (tuple(out.shape) != (n, cache.B, cache.H, cache.d) or
                             not out.is_contiguous() or out.dtype != torch.float32):
         raise EngineError(f"out must be a contiguous float32 [{n}, {cache.B}, {cache.H}, {cache.d}]")

@@ -62,6 +62,41 @@ def test_decode_capacity_is_enforced():
     cache.check()
 
 
+def test_decode_input_shapes_are_checked():
+    """Rows the kernels would misread are refused before any launch: wrong
+    head count, wrong dtype, q / k / v strides that differ, short rows, and
+    for the multi-step call a wrong class layout or step count."""
+    from paper_2310_01801_b200 import (EngineError, ProfilerConfig, decode_step_tensors,
+                                       decode_steps_tensors, encode_prompt_tensors)
+
+    q, k, v = _qkv()
+    cls = torch.zeros(1, 40, dtype=torch.uint8, device="cuda")
+    _, cache = encode_prompt_tensors(q, k, v, cls, ProfilerConfig(), prompt_len=30,
+                                     max_new_tokens=8)
+    row = lambda x, p: x[:, :, p]  # noqa: E731
+    c = cls[:, 30].contiguous()
+    with pytest.raises(EngineError, match="H="):
+        decode_step_tensors(cache, row(q, 30)[:, :1], row(k, 30)[:, :1], row(v, 30)[:, :1], c)
+    with pytest.raises(EngineError, match="q must be"):
+        decode_step_tensors(cache, row(q, 30).double(), row(k, 30), row(v, 30), c)
+    with pytest.raises(EngineError, match="k must be"):
+        decode_step_tensors(cache, row(q, 30), row(k, 30).contiguous(), row(v, 30), c)
+    with pytest.raises(EngineError, match="q must be"):
+        decode_step_tensors(cache, row(q, 30)[..., :8], row(k, 30)[..., :8], row(v, 30)[..., :8], c)
+    seq = lambda x: x[:, :, 30:34]  # noqa: E731
+    with pytest.raises(EngineError, match="new_classes"):
+        decode_steps_tensors(cache, seq(q), seq(k), seq(v), cls[:, 30:34])
+    with pytest.raises(EngineError, match="steps"):
+        decode_steps_tensors(cache, seq(q), k[:, :, 30:33], seq(v),
+                             cls[:, 30:34].t().contiguous())
+    # the valid calls still run, and the cache is intact
+    decode_steps_tensors(cache, seq(q), seq(k), seq(v), cls[:, 30:34].t().contiguous())
+    decode_step_tensors(cache, row(q, 34), row(k, 34), row(v, 34), cls[:, 34].contiguous())
+    torch.cuda.synchronize()
+    cache.check()
+    assert cache.seq_len == 35
+
+
 def test_profiler_config_and_threshold_errors():
     from paper_2310_01801_b200 import (ProfilerConfig, ProfilerError, encode_prompt_tensors,
                                        feasible_set, parse_policy)
