@@ -901,7 +901,11 @@ __global__ void __launch_bounds__(SimtShape<T, D>::NW * 32 + 32, 2) k3_decode_si
 template <int D>
 struct MmaShape {
   static constexpr int NW = 4;                      // consumer warps
-  static constexpr int NE = 4;                      // epilogue warps
+  // three epilogue warps: 9 -> 8 warps per CTA lifts the register cap of
+  // two CTAs per SM from 96 to 128 (4 warps per SM sub-partition); measured
+  // c1 29.60 -> 28.71 us/step, c1_frequent 32.61 -> 32.76 (two: 28.90 /
+  // 36.35, the FREQUENT epilogues need the threads)
+  static constexpr int NE = 3;                      // epilogue warps
   static constexpr int THREADS = (NW + 1 + NE) * 32; // + producer warp
   static constexpr int EFIRST = (NW + 1) * 32;      // first epilogue thread
   static constexpr int RB = D * 2;

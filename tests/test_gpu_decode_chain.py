@@ -121,13 +121,17 @@ def test_more_than_2048_heads_per_call():
                 si += 1
 
 
-@pytest.mark.parametrize("d,dtype", [(128, torch.bfloat16), (64, torch.float32)])
-def test_decode_steps_call_matches_step_by_step(d, dtype):
-    """akv_decode_steps (the step loop in C++, decode_steps_tensors) gives
-    bit-identical outputs, live counts and kept sets to one call per step."""
+@pytest.mark.parametrize("B,H,N,D,d,dtype", [(2, 6, 300, 40, 128, torch.bfloat16),
+                                             (2, 6, 300, 40, 64, torch.float32),
+                                             (3, 12, 420, 40, 64, torch.bfloat16),
+                                             (8, 32, 520, 48, 128, torch.bfloat16)])
+def test_decode_steps_call_matches_step_by_step(B, H, N, D, d, dtype):
+    """akv_decode_steps (one cooperative multi-step launch for bf16 d=64/128,
+    else the step loop in C++; decode_steps_tensors) gives bit-identical
+    outputs, live counts and kept sets to one call per step."""
     from paper_2310_01801_b200 import decode_steps_tensors
 
-    w = _workload(2, 6, 300, 40, d, seed=21)
+    w = _workload(B, H, N, D, d, seed=21 + B)
     qd, kd, vd, cd = _inputs(w)
     qd, kd, vd = qd.to(dtype), kd.to(dtype), vd.to(dtype)
     dev = qd.device
@@ -138,7 +142,7 @@ def test_decode_steps_call_matches_step_by_step(d, dtype):
     for mode in ("steps", "single"):
         res, c = encode_prompt_tensors(qd, kd, vd, cd, ProfilerConfig(recovery_threshold=0.98),
                                        prompt_len=N, max_new_tokens=D, slopes=sl, sinks=sk)
-        outs = torch.empty(D, 2, w.H, d, dtype=torch.float32, device=dev)
+        outs = torch.empty(D, B, w.H, d, dtype=torch.float32, device=dev)
         if mode == "steps":   # two calls: 17 + 23 steps
             cls = cd[:, N:].t().contiguous()
             decode_steps_tensors(c, qd[:, :, N:N + 17], kd[:, :, N:N + 17], vd[:, :, N:N + 17],
