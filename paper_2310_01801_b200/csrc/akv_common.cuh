@@ -139,6 +139,15 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* red, int* total)
   return ex;
 }
 
+// Histogram increment with warp aggregation: the lanes of a warp that hit
+// the same bin (bin < 0: none) add once, by their lowest lane.  Scores of one
+// head share their leading key bytes, so without it every lane of every warp
+// serialises on one shared-memory address in the first radix passes.
+__device__ __forceinline__ void hist_add_agg(int* hist, int bin) {
+  const unsigned peers = __match_any_sync(__activemask(), bin);
+  if (bin >= 0 && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
+}
+
 // ---------------------------------------------------------------------------
 // Exact block-wide top-k over candidates keyed by (score desc, position asc),
 // the order of the reference's stable argsort on -scores (policies.py:238-240).
@@ -152,6 +161,9 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* red, int* total)
 // *thr_key / *thr_pos, the smallest selected (key, pos): candidate i is in the
 // top-k iff key > thr_key || (key == thr_key && pos <= thr_pos).  If k >= n
 // everything is selected (thr_key = 0, thr_pos = INT_MAX).
+// Once the bucket holding the k-th candidate has at most 64 members (after
+// two or three passes for one head's scores, instead of eight), one warp
+// ranks them exactly.
 // `hist` needs 256 ints of shared memory, `red` 33 ints.
 template <typename Sync = BlockSync, typename Get>
 __device__ void block_topk_threshold(int n, int k, Get get, int* hist, int* red,
@@ -162,8 +174,9 @@ __device__ void block_topk_threshold(int n, int k, Get get, int* hist, int* red,
     *thr_pos = 0x7fffffff;
     return;
   }
-  __shared__ unsigned long long s_prefix;
-  __shared__ int s_remain, s_digit;
+  constexpr int kSmall = 64;
+  __shared__ unsigned long long s_prefix, s_ck[kSmall], s_tk;
+  __shared__ int s_remain, s_digit, s_bucket, s_cn, s_cp[kSmall], s_tp;
   if (tid == 0) { s_prefix = 0ull; s_remain = k; }
   Sync::sync();
   unsigned long long mask = 0ull;
@@ -174,7 +187,7 @@ __device__ void block_topk_threshold(int n, int k, Get get, int* hist, int* red,
     for (int i = tid; i < n; i += nth) {
       unsigned long long key; int pos;
       get(i, &key, &pos);
-      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 0xff], 1);
+      hist_add_agg(hist, (key & mask) == prefix ? (int)((key >> shift) & 0xff) : -1);
     }
     Sync::sync();
     if (tid < 32) {
@@ -191,25 +204,69 @@ __device__ void block_topk_threshold(int n, int k, Get get, int* hist, int* red,
       }
       int before = incl - s;  // elements with larger digits than my first bin
       const int remain = s_remain;
-      int found = -1, above = 0;
+      int found = -1, above = 0, fcnt = 0;
       int run = before;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        if (found < 0 && run < remain && run + c[j] >= remain) { found = 255 - (lane * 8 + j); above = run; }
+        if (found < 0 && run < remain && run + c[j] >= remain) { found = 255 - (lane * 8 + j); above = run; fcnt = c[j]; }
         run += c[j];
       }
       unsigned ball = __ballot_sync(0xffffffffu, found >= 0);
       int src = __ffs(ball) - 1;
       int dg = __shfl_sync(0xffffffffu, found, src);
       int ab = __shfl_sync(0xffffffffu, above, src);
+      int bc = __shfl_sync(0xffffffffu, fcnt, src);
       if (lane == 0) {
         s_digit = dg;
         s_remain = remain - ab;
         s_prefix = prefix | ((unsigned long long)dg << shift);
+        s_bucket = bc;
+        s_cn = 0;
       }
     }
     Sync::sync();
     mask |= (0xffull << shift);
+    if (s_bucket <= kSmall) break;
+  }
+  if (s_bucket <= kSmall) {
+    // gather the bucket, rank it in one warp: the candidate ranked need-1
+    // (key desc, position asc) is the smallest selected one
+    const unsigned long long bp = s_prefix;
+    for (int i = tid; i < n; i += nth) {
+      unsigned long long key; int pos;
+      get(i, &key, &pos);
+      if ((key & mask) == bp) {
+        const int slot = atomicAdd(&s_cn, 1);
+        s_ck[slot] = key;
+        s_cp[slot] = pos;
+      }
+    }
+    Sync::sync();
+    if (tid < 32) {
+      const int lane = tid, m = s_cn, need = s_remain;
+      const unsigned long long k0 = lane < m ? s_ck[lane] : 0ull, k1 = lane + 32 < m ? s_ck[lane + 32] : 0ull;
+      const int p0 = lane < m ? s_cp[lane] : 0, p1 = lane + 32 < m ? s_cp[lane + 32] : 0;
+      int r0 = 0, r1 = 0;
+      for (int o = 0; o < m; ++o) {
+        const unsigned long long ko = s_ck[o];
+        const int po = s_cp[o];
+        r0 += (ko > k0 || (ko == k0 && po < p0));
+        r1 += (ko > k1 || (ko == k1 && po < p1));
+      }
+      const unsigned b0 = __ballot_sync(0xffffffffu, lane < m && r0 == need - 1);
+      const unsigned b1 = __ballot_sync(0xffffffffu, lane + 32 < m && r1 == need - 1);
+      const int src = b0 ? __ffs(b0) - 1 : __ffs(b1) - 1;
+      const unsigned long long tk = __shfl_sync(0xffffffffu, b0 ? k0 : k1, src);
+      const int tp = __shfl_sync(0xffffffffu, b0 ? p0 : p1, src);
+      // every candidate equal to the threshold value selected: open position bound
+      const bool more = (lane < m && k0 == tk && p0 > tp) || (lane + 32 < m && k1 == tk && p1 > tp);
+      const bool any = __any_sync(0xffffffffu, more);
+      if (lane == 0) { s_tk = tk; s_tp = any ? tp : 0x7fffffff; }
+    }
+    Sync::sync();
+    *thr_key = s_tk;
+    *thr_pos = s_tp;
+    return;
   }
   const unsigned long long vstar = s_prefix;
   const int need_eq = s_remain;  // how many elements equal to v* are selected (>= 1)
@@ -246,7 +303,7 @@ __device__ void block_topk_threshold(int n, int k, Get get, int* hist, int* red,
       unsigned long long key; int pos;
       get(i, &key, &pos);
       int ip = kPosMask - pos;
-      if (key == vstar && (ip & pmask) == prefix) atomicAdd(&hist[(ip >> shift) & 0xff], 1);
+      hist_add_agg(hist, (key == vstar && (ip & pmask) == prefix) ? ((ip >> shift) & 0xff) : -1);
     }
     Sync::sync();
     if (tid == 0) {

@@ -286,24 +286,75 @@ struct PolicyParams {
 };
 
 constexpr int kPolicyThreads = 512;
+#ifdef AKV_TRACE_POL
+__device__ unsigned long long g_pol_trace[4096][8];
+#define POL_STAMP(i) do { if (threadIdx.x == 0 && blockIdx.x < 4096) g_pol_trace[blockIdx.x][i] = clock64(); } while (0)
+extern "C" int akv_debug_pol_trace(void* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_pol_trace, sizeof(g_pol_trace));
+}
+#else
+#define POL_STAMP(i) do {} while (0)
+#endif
+// per-key bytes staged in shared memory (score key, colsq, lastp, class) and
+// the largest prompt staged; longer prompts read the global arrays
+constexpr int kPolicyStageBytes = 8 + 8 + 4 + 1;
+constexpr int kPolicyStageMaxN = 7680;
 
-__global__ void __launch_bounds__(kPolicyThreads) k1_policy(PolicyParams p) {
+// One CTA per head.  The head's per-key inputs are staged in shared memory
+// once, so the top-k radix passes and the member passes touch no global
+// memory; every family member's recovery, cost and cosine come from ONE pass
+// over the keys with per-member register accumulators and one combined
+// reduction (the per-thread strided sums and the warp-tree / warp-order
+// combine are those of block_sum, so the results are unchanged bit for bit).
+__global__ void __launch_bounds__(kPolicyThreads, 2) k1_policy(PolicyParams p) {
+  extern __shared__ __align__(16) uint8_t s_stage[];
   __shared__ int hist[256];
   __shared__ int red_i[33];
   __shared__ double red_d[kPolicyThreads / 32];
   __shared__ unsigned long long s_thr_key[AKV_MAX_FAMILY];
   __shared__ int s_thr_pos[AKV_MAX_FAMILY];
+  __shared__ int s_loc[AKV_MAX_FAMILY];
   __shared__ int s_choice[AKV_MAX_THRESHOLDS];
+  __shared__ double s_rs[kPolicyThreads / 32][AKV_MAX_FAMILY + 1], s_qs[kPolicyThreads / 32][AKV_MAX_FAMILY];
+  __shared__ int s_cn[kPolicyThreads / 32][AKV_MAX_FAMILY];
+  // launched programmatically after the tensor-core passes: their outputs
+  // are complete past this point (a no-op after an ordinary launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int g = blockIdx.x;
   const int b = g / p.H;
   const int N = p.N;
-  const uint8_t* cls = p.cls + (size_t)b * p.cls_ld;
-  const double* colsum = p.colsum + (size_t)g * N;
-  const double* colsq = p.colsq + (size_t)g * N;
-  const float* lastp = p.lastp + (size_t)g * N;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NWP = kPolicyThreads / 32;
+  const uint8_t* cls_g = p.cls + (size_t)b * p.cls_ld;
+  const double* colsum_g = p.colsum + (size_t)g * N;
+  const double* colsq_g = p.colsq + (size_t)g * N;
+  const float* lastp_g = p.lastp + (size_t)g * N;
+  const bool staged = N <= kPolicyStageMaxN;
+  unsigned long long* s_key = reinterpret_cast<unsigned long long*>(s_stage);
+  double* s_sq = reinterpret_cast<double*>(s_key + N);
+  float* s_lp = reinterpret_cast<float*>(s_sq + N);
+  uint8_t* s_cls = reinterpret_cast<uint8_t*>(s_lp + N);
+  POL_STAMP(0);
+  if (staged) {
+    for (int j = tid; j < N; j += kPolicyThreads) {
+      s_key[j] = score_key(colsum_g[j]);
+      s_sq[j] = colsq_g[j];
+      s_lp[j] = lastp_g[j];
+      s_cls[j] = cls_g[j];
+    }
+  }
+  if (tid < p.n_family) s_loc[tid] = N - budget(p.r_l[tid], p.local_len);
+  __syncthreads();
+  POL_STAMP(1);
+  auto key_at = [&](int j) { return staged ? s_key[j] : score_key(colsum_g[j]); };
+  auto sq_at = [&](int j) { return staged ? s_sq[j] : colsq_g[j]; };
+  auto lp_at = [&](int j) { return staged ? s_lp[j] : lastp_g[j]; };
+  auto cls_at = [&](int j) { return staged ? (int)s_cls[j] : (int)cls_g[j]; };
+  // the staged key is the score with -0.0 folded onto +0.0: the same sums
+  auto cs_at = [&](int j) { return staged ? __longlong_as_double((long long)s_key[j]) : colsum_g[j]; };
 
   auto get = [&](int i, unsigned long long* key, int* pos) {
-    *key = score_key(colsum[i]);
+    *key = key_at(i);
     *pos = i;
   };
   // exact frequent top-k thresholds (one per member with FREQUENT), and the
@@ -311,24 +362,24 @@ __global__ void __launch_bounds__(kPolicyThreads) k1_policy(PolicyParams p) {
   // One radix select per distinct frequent budget (members sharing r_f share
   // the threshold); the (k+1)-th largest key for the gap is the largest key
   // outside the selected set - a block max, not a second select.
-  __shared__ unsigned long long s_next[kPolicyThreads / 32];
+  __shared__ unsigned long long s_next[NWP];
   double min_gap = INFINITY;
   int have = -1;  // a member whose threshold is already in s_thr_*
   for (int f = 0; f < p.n_family; ++f) {
     if (!(p.atoms[f] & AKV_ATOM_FREQUENT) || (p.atoms[f] & AKV_ATOM_FULL)) continue;
     if (have >= 0 && p.r_f[have] == p.r_f[f]) {
-      if (threadIdx.x == 0) { s_thr_key[f] = s_thr_key[have]; s_thr_pos[f] = s_thr_pos[have]; }
+      if (tid == 0) { s_thr_key[f] = s_thr_key[have]; s_thr_pos[f] = s_thr_pos[have]; }
       __syncthreads();
       continue;
     }
     const int kb = budget(p.r_f[f], N);
     unsigned long long tk; int tp;
     block_topk_threshold(N, kb, get, hist, red_i, &tk, &tp);
-    if (threadIdx.x == 0) { s_thr_key[f] = tk; s_thr_pos[f] = tp; }
+    if (tid == 0) { s_thr_key[f] = tk; s_thr_pos[f] = tp; }
     if (kb < N) {
       unsigned long long nk = 0ull;
-      for (int j = threadIdx.x; j < N; j += blockDim.x) {
-        const unsigned long long key = score_key(colsum[j]);
+      for (int j = tid; j < N; j += kPolicyThreads) {
+        const unsigned long long key = key_at(j);
         if (!topk_selected(key, j, tk, tp) && key > nk) nk = key;
       }
 #pragma unroll
@@ -336,10 +387,10 @@ __global__ void __launch_bounds__(kPolicyThreads) k1_policy(PolicyParams p) {
         const unsigned long long other = __shfl_xor_sync(0xffffffffu, nk, o);
         nk = other > nk ? other : nk;
       }
-      if ((threadIdx.x & 31) == 0) s_next[threadIdx.x >> 5] = nk;
+      if (lane == 0) s_next[warp] = nk;
       __syncthreads();
       nk = 0ull;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) nk = s_next[w] > nk ? s_next[w] : nk;
+      for (int w = 0; w < NWP; ++w) nk = s_next[w] > nk ? s_next[w] : nk;
       const double a = __longlong_as_double(tk), c = __longlong_as_double(nk);
       const double gap = a > 0.0 ? (a - c) / a : 0.0;
       min_gap = fmin(min_gap, gap);
@@ -349,49 +400,68 @@ __global__ void __launch_bounds__(kPolicyThreads) k1_policy(PolicyParams p) {
   }
   __syncthreads();
 
-  auto kept = [&](int f, int j) -> bool {
+  POL_STAMP(2);
+  auto kept = [&](int f, int j, unsigned long long key, int c) -> bool {
     const uint8_t at = p.atoms[f];
     if (at & AKV_ATOM_FULL) return true;
-    const int c = cls[j];
     bool k = ((at & AKV_ATOM_SPECIAL) && c == AKV_CLS_SPECIAL) ||
              ((at & AKV_ATOM_PUNCT) && c == AKV_CLS_PUNCT);
-    if (at & AKV_ATOM_LOCAL) k |= j >= N - budget(p.r_l[f], p.local_len);
-    if (at & AKV_ATOM_FREQUENT)
-      k |= topk_selected(score_key(colsum[j]), j, s_thr_key[f], s_thr_pos[f]);
+    if (at & AKV_ATOM_LOCAL) k |= j >= s_loc[f];
+    if (at & AKV_ATOM_FREQUENT) k |= topk_selected(key, j, s_thr_key[f], s_thr_pos[f]);
     return k;
   };
 
-  // colsq total for the cosine criterion
-  double tot_sq = 0.0;
-  for (int j = threadIdx.x; j < N; j += blockDim.x) tot_sq += colsq[j];
-  tot_sq = block_sum(tot_sq, red_d);
-
-  for (int f = 0; f < p.n_family; ++f) {
-    double rsum = 0.0, qsum = 0.0;
-    int cnt = 0;
-    for (int j = threadIdx.x; j < N; j += blockDim.x) {
-      if (kept(f, j)) {
-        rsum += (p.rows == AKV_ROWS_LAST) ? (double)lastp[j] : colsum[j];
-        qsum += colsq[j];
-        ++cnt;
+  // every member's kept mass (colsum or last row), colsq mass and count, and
+  // the colsq total for the cosine criterion: per member one pass over the
+  // staged keys and a warp reduction, then ONE block barrier for them all
+  {
+    const bool last = p.rows == AKV_ROWS_LAST;
+    double tot = 0.0;
+    for (int j = tid; j < N; j += kPolicyThreads) tot += sq_at(j);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (lane == 0) s_rs[warp][AKV_MAX_FAMILY] = tot;
+    for (int f = 0; f < p.n_family; ++f) {
+      double rs = 0.0, qs = 0.0;
+      int cn = 0;
+      for (int j = tid; j < N; j += kPolicyThreads) {
+        if (kept(f, j, key_at(j), cls_at(j))) {
+          rs += last ? (double)lp_at(j) : cs_at(j);
+          qs += sq_at(j);
+          ++cn;
+        }
       }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        rs += __shfl_xor_sync(0xffffffffu, rs, o);
+        qs += __shfl_xor_sync(0xffffffffu, qs, o);
+        cn += __shfl_xor_sync(0xffffffffu, cn, o);
+      }
+      if (lane == 0) { s_rs[warp][f] = rs; s_qs[warp][f] = qs; s_cn[warp][f] = cn; }
     }
-    rsum = block_sum(rsum, red_d);
-    qsum = block_sum(qsum, red_d);
-    cnt = block_sum(cnt, red_i);
-    if (threadIdx.x == 0) {
+    __syncthreads();
+    if (tid < p.n_family) {
+      const int f = tid;
+      double rsum = 0.0, qsum = 0.0, tot_sq = 0.0;
+      int cnt = 0;
+      for (int w = 0; w < NWP; ++w) {
+        rsum += s_rs[w][f];
+        qsum += s_qs[w][f];
+        cnt += s_cn[w][f];
+        tot_sq += s_rs[w][AKV_MAX_FAMILY];
+      }
       double R;
       if (p.atoms[f] & AKV_ATOM_FULL) R = 1.0;  // A's rows sum to 1 exactly
       else if (cnt == 0) R = 0.0;               // profiler.py:82-83
-      else R = (p.rows == AKV_ROWS_LAST) ? rsum : rsum / (double)N;
+      else R = last ? rsum : rsum / (double)N;
       p.recovery[(size_t)g * p.n_family + f] = R;
       p.cost[(size_t)g * p.n_family + f] = cnt;
-      double cs = (p.atoms[f] & AKV_ATOM_FULL) ? 1.0 : (qsum == 0.0 ? 0.0 : sqrt(qsum) / sqrt(tot_sq));
+      const double cs = (p.atoms[f] & AKV_ATOM_FULL) ? 1.0 : (qsum == 0.0 ? 0.0 : sqrt(qsum) / sqrt(tot_sq));
       p.cosine[(size_t)g * p.n_family + f] = cs;
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     const double* R = p.recovery + (size_t)g * p.n_family;
     const double* cs = p.cosine + (size_t)g * p.n_family;
     for (int t = 0; t < p.n_thr; ++t) {
@@ -410,23 +480,25 @@ __global__ void __launch_bounds__(kPolicyThreads) k1_policy(PolicyParams p) {
     p.topk_gap[g] = min_gap;
   }
   __syncthreads();
+  POL_STAMP(3);
   const int f0 = s_choice[0];
   // ordered kept positions of the primary choice: each thread owns a
   // contiguous range of positions
-  const int per = (N + blockDim.x - 1) / blockDim.x;
-  const int lo = min(N, (int)threadIdx.x * per), hi = min(N, lo + per);
+  const int per = (N + kPolicyThreads - 1) / kPolicyThreads;
+  const int lo = min(N, tid * per), hi = min(N, lo + per);
   int mine = 0;
   double lr = 0.0;
   if (f0 >= 0)
     for (int j = lo; j < hi; ++j)
-      if (kept(f0, j)) { ++mine; lr += (double)lastp[j]; }
+      if (kept(f0, j, key_at(j), cls_at(j))) { ++mine; lr += (double)lp_at(j); }
   int total;
   int off = block_exclusive_scan(mine, red_i, &total);
   if (f0 >= 0)
     for (int j = lo; j < hi; ++j)
-      if (kept(f0, j)) p.kept_pos[(size_t)g * N + off++] = j;
+      if (kept(f0, j, key_at(j), cls_at(j))) p.kept_pos[(size_t)g * N + off++] = j;
+  POL_STAMP(4);
   lr = block_sum(lr, red_d);
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     p.kept_count[g] = f0 >= 0 ? total : 0;
     p.last_row_recovery[g] = f0 >= 0 ? lr : 0.0;
     // initial frequent set of the chosen policy (decode's incremental top-k)
@@ -434,12 +506,14 @@ __global__ void __launch_bounds__(kPolicyThreads) k1_policy(PolicyParams p) {
     p.thr_key[g] = fr ? s_thr_key[f0] : ~0ull;
     p.thr_pos[g] = fr ? s_thr_pos[f0] : -1;
   }
+  POL_STAMP(5);
   // pending output A[N-1] @ V = sum of the per-key-tile partials
-  for (int c = threadIdx.x; c < p.d; c += blockDim.x) {
+  for (int c = tid; c < p.d; c += kPolicyThreads) {
     float o = 0.f;
     for (int t = 0; t < p.ntiles; ++t) o += p.out_part[((size_t)g * p.ntiles + t) * p.d + c];
     p.out_last[(size_t)g * p.d + c] = o;
   }
+  POL_STAMP(6);
 }
 
 template <typename T, int D>
@@ -460,6 +534,12 @@ static cudaError_t launch_simt_passes(const ProfParams& pp, int G, int ntiles, c
 }  // namespace akv
 
 using namespace akv;
+
+// the policy epilogue launches programmatically (AKV_K1_POLICY_PDL=0: ordinary launch, A/B)
+static bool k1_policy_pdl() {
+  static const bool v = [] { const char* e = getenv("AKV_K1_POLICY_PDL"); return !e || atoi(e) != 0; }();
+  return v;
+}
 
 extern "C" size_t akv_profile_workspace_size(int32_t B, int32_t H, int32_t N, int32_t d) {
   const size_t ntiles = (size_t)(N + kTile - 1) / kTile;
@@ -542,7 +622,27 @@ extern "C" int akv_profile(const akv_profile_args* a, void* stream) {
   pol.thr_pos = a->topk_thr_pos_dev;
   if (!pol.thr_key || !pol.thr_pos)
     return set_error(AKV_ERR_INVALID, "akv_profile: topk threshold outputs are required");
-  k1_policy<<<G, kPolicyThreads, 0, st>>>(pol);
+  static PerDeviceOnce pol_attr;
+  e = pol_attr.run([](int) {
+    return cudaFuncSetAttribute(k1_policy, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kPolicyStageMaxN * kPolicyStageBytes);
+  });
+  if (e != cudaSuccess) return set_error(AKV_ERR_CUDA, "akv_profile policy: %s", cudaGetErrorString(e));
+  const size_t pol_smem = a->N <= kPolicyStageMaxN ? (size_t)a->N * kPolicyStageBytes : 0;
+  {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(kPolicyThreads);
+    cfg.dynamicSmemBytes = pol_smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = k1_policy_pdl() ? 1 : 0;
+    e = cudaLaunchKernelEx(&cfg, k1_policy, pol);
+    if (e != cudaSuccess) return set_error(AKV_ERR_CUDA, "akv_profile policy: %s", cudaGetErrorString(e));
+  }
   e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(AKV_ERR_CUDA, "akv_profile policy: %s", cudaGetErrorString(e));
   return AKV_OK;

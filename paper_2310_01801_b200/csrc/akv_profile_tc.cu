@@ -345,6 +345,10 @@ __global__ void __launch_bounds__(kTcThreads, 2)
       for (int j = 0; j < nitems; ++j) {
         const int kt = item_kt(j), nq = ntiles - kt;
         const int rk = (int)((int64_t)g * p.ld + (int64_t)kt * kTT);
+        // the key tile's V rows, read by the epilogue's last-row partial at
+        // the item's end: into L2 now
+        bulk_prefetch_l2(p.v + ((size_t)g * p.ld + (size_t)kt * kTT) * 128,
+                         (uint32_t)min(kTT, p.N - kt * kTT) * 256u);
         mbar_wait(&k_empty, (j & 1) ^ 1);  // the previous item's MMAs have read sK
         mbar_arrive_expect_tx(&k_full, kTileB);
         tma_load_2d(sK, &tmK, 0, rk, &k_full, pol_k);

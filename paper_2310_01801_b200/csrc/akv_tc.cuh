@@ -185,8 +185,12 @@ __device__ __forceinline__ uint64_t f2_exp2_fma(uint64_t x2) {
 // FMA pipe: every kPolyEvery-th pair, 0 = none.  Measured at config 4 (B200):
 // row pass 5.67 -> 5.40 ms with a quarter on the FMA pipe; neither the MUFU
 // (XU ~60 %) nor the issue slots (~64 %) saturate - the epilogue is latency
-// bound at 16 epilogue warps per SM.
-constexpr int kPolyEvery = 4;
+// bound at 16 epilogue warps per SM.  An eighth (kPolyEvery 8): K1 at config 1
+// 0.2013 -> 0.1981 ms, config 4 unchanged (2 of 8 on the FMA pipe: slower).
+#ifndef AKV_POLY_EVERY
+#define AKV_POLY_EVERY 8
+#endif
+constexpr int kPolyEvery = AKV_POLY_EVERY;
 
 __device__ __forceinline__ float exp2_mixed(float x, int c) {
   return (kPolyEvery > 0 && c % (kPolyEvery > 0 ? kPolyEvery : 1) == kPolyEvery - 1)
