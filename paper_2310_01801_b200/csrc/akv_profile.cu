@@ -317,6 +317,7 @@ __global__ void __launch_bounds__(kPolicyThreads, 2) k1_policy(PolicyParams p) {
   __shared__ int s_choice[AKV_MAX_THRESHOLDS];
   __shared__ double s_rs[kPolicyThreads / 32][AKV_MAX_FAMILY + 1], s_qs[kPolicyThreads / 32][AKV_MAX_FAMILY];
   __shared__ int s_cn[kPolicyThreads / 32][AKV_MAX_FAMILY];
+  __shared__ double s_R[AKV_MAX_FAMILY], s_cs[AKV_MAX_FAMILY];
   // launched programmatically after the tensor-core passes: their outputs
   // are complete past this point (a no-op after an ordinary launch)
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -455,15 +456,17 @@ __global__ void __launch_bounds__(kPolicyThreads, 2) k1_policy(PolicyParams p) {
       else if (cnt == 0) R = 0.0;               // profiler.py:82-83
       else R = last ? rsum : rsum / (double)N;
       p.recovery[(size_t)g * p.n_family + f] = R;
+      s_R[f] = R;
       p.cost[(size_t)g * p.n_family + f] = cnt;
       const double cs = (p.atoms[f] & AKV_ATOM_FULL) ? 1.0 : (qsum == 0.0 ? 0.0 : sqrt(qsum) / sqrt(tot_sq));
       p.cosine[(size_t)g * p.n_family + f] = cs;
+      s_cs[f] = cs;
     }
   }
   __syncthreads();
   if (tid == 0) {
-    const double* R = p.recovery + (size_t)g * p.n_family;
-    const double* cs = p.cosine + (size_t)g * p.n_family;
+    const double* R = s_R;  // this block's values: no global round trip per member
+    const double* cs = s_cs;
     for (int t = 0; t < p.n_thr; ++t) {
       int c = -1;
       if (p.criterion == AKV_CRIT_COSINE) {
