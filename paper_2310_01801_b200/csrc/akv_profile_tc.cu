@@ -34,7 +34,10 @@ constexpr int kTT = 128;                   // tile edge (queries / keys)
 constexpr int kBoxB = 128 * 128;           // one 128-row x 64-col bf16 box (16 KB)
 constexpr int kTileB = 2 * kBoxB;          // 128 x 128 bf16 tile (32 KB)
 constexpr int kRing = 2;                   // streamed-operand stages
-constexpr int kGroups = 2;                 // epilogue column groups (4 warps = 128 TMEM lanes each)
+#ifndef AKV_K1_GROUPS
+#define AKV_K1_GROUPS 2
+#endif
+constexpr int kGroups = AKV_K1_GROUPS;     // epilogue column groups (4 warps = 128 TMEM lanes each)
 constexpr int kCols = 128 / kGroups;       // accumulator columns per epilogue thread and tile
 constexpr int kEpiWarps = 4 * kGroups;
 constexpr int kTcThreads = 64 + 32 * kEpiWarps;  // warp0 TMA, warp1 MMA/TMEM, then the epilogue
@@ -63,7 +66,8 @@ using EpiSync = NamedSync<32 * kEpiWarps, 1, 64>;
 
 // kCols consecutive fp32 accumulator columns of this thread's TMEM lane
 __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float* v) {
-  if constexpr (kCols == 64) tmem_ld64(taddr, v);
+  if constexpr (kCols == 128) tmem_ld128(taddr, v);
+  else if constexpr (kCols == 64) tmem_ld64(taddr, v);
   else tmem_ld32(taddr, v);
 }
 
@@ -514,8 +518,8 @@ __global__ void __launch_bounds__(kTcThreads, 2)
         // epilogue threads: 16-byte loads of 8 dims, every load in flight at
         // once (a per-dimension loop here was a chain of ~30 L2/DRAM round
         // trips at the end of every CTA); partials meet in s_red
-        static_assert(kTT * 128 / 8 == 8 * 32 * kEpiWarps, "16-byte loads per epilogue thread");
-        constexpr int RG = 32 * kEpiWarps / 16;  // row groups
+        constexpr int RG = 32 * kEpiWarps / 16;  // row groups (16 threads cover a 128-dim row)
+        static_assert(kTT % RG == 0, "row groups tile the key tile");
         const __nv_bfloat16* vt = p.v + ((size_t)g * p.ld + (size_t)kt * kTT) * 128;
         const int nrow = min(kTT, p.N - kt * kTT);
         const int c = et & 15, r0 = et >> 4;

@@ -92,11 +92,24 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, float* v) {
       : "r"(taddr + (OFF)))
   AKV_LD32(0, r);
   AKV_LD32(32, (r + 32));
-#undef AKV_LD32
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
 }
+
+// 128 consecutive fp32 columns (a full 128-wide accumulator row): four x32
+// loads in flight behind one wait
+__device__ __forceinline__ void tmem_ld128(uint32_t taddr, float* v) {
+  uint32_t r[128];
+  AKV_LD32(0, r);
+  AKV_LD32(32, (r + 32));
+  AKV_LD32(64, (r + 64));
+  AKV_LD32(96, (r + 96));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 128; ++i) v[i] = __uint_as_float(r[i]);
+}
+#undef AKV_LD32
 
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
