@@ -4,7 +4,7 @@ buffer per step): when each step's CTAs start, land their first page, finish
 streaming and finish publishing, relative to the first CTA of the first
 traced step - how much of a step overlaps its predecessor.
 
-    python tools/k3_timeline.py [config] [T] [steps]
+    python tools/k3_timeline.py [config] [T] [steps] [B]
 """
 import ctypes
 import os
@@ -26,7 +26,7 @@ def main():
     T = float(sys.argv[2]) if len(sys.argv) > 2 else 0.95
     n = int(sys.argv[3]) if len(sys.argv) > 3 else 4
     dev = torch.device("cuda")
-    w = CONFIGS[name]()
+    w = CONFIGS[name](B=int(sys.argv[4])) if len(sys.argv) > 4 else CONFIGS[name]()
     qd, kd, vd, cd, *_ = bench.make_inputs(w, dev)
     sl = torch.tensor(w.slopes, dtype=torch.float32, device=dev)
     sk = torch.tensor(w.sinks, dtype=torch.float32, device=dev)
