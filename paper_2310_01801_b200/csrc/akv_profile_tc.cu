@@ -33,7 +33,13 @@ namespace akv {
 constexpr int kTT = 128;                   // tile edge (queries / keys)
 constexpr int kBoxB = 128 * 128;           // one 128-row x 64-col bf16 box (16 KB)
 constexpr int kTileB = 2 * kBoxB;          // 128 x 128 bf16 tile (32 KB)
-constexpr int kRing = 2;                   // streamed-operand stages
+#ifndef AKV_K1_RING
+#define AKV_K1_RING 2
+#endif
+#ifndef AKV_K1_CTAS_PER_SM
+#define AKV_K1_CTAS_PER_SM 2
+#endif
+constexpr int kRing = AKV_K1_RING;         // streamed-operand stages
 #ifndef AKV_K1_GROUPS
 #define AKV_K1_GROUPS 2
 #endif
@@ -134,7 +140,7 @@ __device__ __forceinline__ void row_update_raw(const float* v, float sl2, float&
 // tensor-map prefetch serve both items, the second item's Q tile loads as
 // soon as the first item's last MMA has read sQ, and all ring / accumulator
 // phases run on per-CTA counters.
-__global__ void __launch_bounds__(kTcThreads, 2)
+__global__ void __launch_bounds__(kTcThreads, AKV_K1_CTAS_PER_SM)
     k1tc_rowlse(const __grid_constant__ TcParams p, const __grid_constant__ CUtensorMap tmQ,
                 const __grid_constant__ CUtensorMap tmK) {
   extern __shared__ uint8_t smem_raw[];
@@ -308,7 +314,7 @@ __global__ void __launch_bounds__(kTcThreads, 2)
 // (key tile x, ntiles-x query tiles) is the heavier one.
 constexpr size_t kTcSmemCol = kTcSmem + (size_t)(32 * kEpiWarps / 16) * 128 * 4;  // + out_part scratch
 
-__global__ void __launch_bounds__(kTcThreads, 2)
+__global__ void __launch_bounds__(kTcThreads, AKV_K1_CTAS_PER_SM)
     k1tc_colsum(const __grid_constant__ TcParams p, const __grid_constant__ CUtensorMap tmQ,
                 const __grid_constant__ CUtensorMap tmK) {
   extern __shared__ uint8_t smem_raw[];
