@@ -1323,6 +1323,7 @@ static int k3_grid(int sms) {
   return v > 0 ? v : 2 * sms;
 }
 unsigned long long* g_dec_trace = nullptr;  // set by akv_debug_set_decode_trace
+int g_dec_trace_ring = 1;                    // consecutive steps to keep apart (trace ring)
 // consumers publish the CTA's last segment (AKV_K3_CONSUMER_TAIL, tuning)
 static int k3_consumer_tail() {
   static const int v = env_int("AKV_K3_CONSUMER_TAIL", 1) != 0;
@@ -1511,6 +1512,14 @@ using namespace akv;
 // the next decode launches into a device buffer of [2*SMs, 16] uint64.
 extern "C" void akv_debug_set_decode_trace(void* buf) {
   g_dec_trace = static_cast<unsigned long long*>(buf);
+  g_dec_trace_ring = 1;
+}
+
+// The same, for n consecutive steps kept apart: step s records into block
+// (s mod n) of a buffer of n x [2*SMs, 16] uint64 (decode_steps runs).
+extern "C" void akv_debug_set_decode_trace_ring(void* buf, int n) {
+  g_dec_trace = static_cast<unsigned long long*>(buf);
+  g_dec_trace_ring = n > 1 ? n : 1;
 }
 
 extern "C" size_t akv_decode_workspace_size(int32_t B, int32_t H, int32_t d, int32_t max_cap,
@@ -1526,6 +1535,14 @@ extern "C" int akv_decode_workspace_init(void* ws, size_t bytes, int32_t B, int3
                                   static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return set_error(AKV_ERR_CUDA, "akv_decode_workspace_init: %s", cudaGetErrorString(e));
   return AKV_OK;
+}
+
+static unsigned long long* trace_for(const akv_decode_args* a) {
+  if (!g_dec_trace || g_dec_trace_ring <= 1) return g_dec_trace;
+  int sms = 0;
+  if (current_sm_count(&sms) != cudaSuccess) return g_dec_trace;
+  const int slot = (a->pos - a->prompt_len) % g_dec_trace_ring;
+  return g_dec_trace + (size_t)slot * 2 * sms * 16;
 }
 
 extern "C" int akv_decode_step(const akv_decode_args* a, void* stream) {
@@ -1573,7 +1590,7 @@ extern "C" int akv_decode_step(const akv_decode_args* a, void* stream) {
                 a->live_out_dev + g0, a->out_dev + g0 * a->d, at(a->evicted_dev, g0),
                 a->status_dev ? a->status_dev : w.status,
                 w.part + g0 * w.max_parts * (a->d + 2), w.logit, w.counter + g0, w.max_parts, scale,
-                g_dec_trace, a->pos_dev, a->flags, at(a->lse_out_dev, g0), a->peer_out_dev,
+                trace_for(a), a->pos_dev, a->flags, at(a->lse_out_dev, g0), a->peer_out_dev,
                 a->n_peers, a->peer_ld, a->peer_col0 + (int64_t)b0 * a->peer_ld,
                 a->dtype == AKV_DTYPE_BF16, k3_l2_prefetch(), k3_consumer_tail()};
     if (a->dtype == AKV_DTYPE_BF16) {

@@ -4,7 +4,11 @@ buffer per step): when each step's CTAs start, land their first page, finish
 streaming and finish publishing, relative to the first CTA of the first
 traced step - how much of a step overlaps its predecessor.
 
-    python tools/k3_timeline.py [config] [T] [steps] [B]
+    python tools/k3_timeline.py [config] [T] [steps] [B] [call]
+
+call = "step" (one decode_step_tensors call per step, the default) or
+"steps" (one decode_steps_tensors call for the traced steps: the step loop
+in C++, as bench sessions issue them; a trace ring keeps the steps apart).
 """
 import ctypes
 import os
@@ -16,7 +20,8 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import bench  # noqa: E402
-from paper_2310_01801_b200 import ProfilerConfig, decode_step_tensors, encode_prompt_tensors  # noqa: E402
+from paper_2310_01801_b200 import (ProfilerConfig, decode_step_tensors,  # noqa: E402
+                                   decode_steps_tensors, encode_prompt_tensors)
 from paper_2310_01801_b200._lib import lib  # noqa: E402
 from paper_2310_01801_b200.workloads import CONFIGS  # noqa: E402
 
@@ -37,13 +42,30 @@ def main():
     _, c = encode_prompt_tensors(qd, kd, vd, cd, ProfilerConfig(recovery_threshold=T),
                                  prompt_len=w.N, max_new_tokens=w.D, slopes=sl, sinks=sk)
     at = w.D // 2
-    for t in range(at + n):
-        if t >= at:
-            lib.akv_debug_set_decode_trace(bufs[t - at].data_ptr())
-        decode_step_tensors(c, dec[0][t], dec[1][t], dec[2][t], dec[3][t], chained=True)
-    lib.akv_debug_set_decode_trace(None)
-    torch.cuda.synchronize()
-    trs = [b.view(-1, 16).cpu().numpy().astype(np.float64) for b in bufs]
+    call = sys.argv[5] if len(sys.argv) > 5 else "step"
+    if call == "steps":
+        for t in range(at):
+            decode_step_tensors(c, dec[0][t], dec[1][t], dec[2][t], dec[3][t], chained=True)
+        ring = torch.zeros(n * 2 * sms * 16, dtype=torch.int64, device=dev)
+        lib.akv_debug_set_decode_trace_ring.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        lib.akv_debug_set_decode_trace_ring(ring.data_ptr(), n)
+        N = w.N
+        cls = cd[:, N + at:N + at + n].t().contiguous()
+        decode_steps_tensors(c, qd[:, :, N + at:N + at + n], kd[:, :, N + at:N + at + n],
+                             vd[:, :, N + at:N + at + n], cls, chained=True)
+        lib.akv_debug_set_decode_trace(None)
+        torch.cuda.synchronize()
+        # step s of the call wrote block (at + s) mod n
+        blocks = ring.view(n, -1, 16).cpu().numpy().astype(np.float64)
+        trs = [blocks[(at + s) % n] for s in range(n)]
+    else:
+        for t in range(at + n):
+            if t >= at:
+                lib.akv_debug_set_decode_trace(bufs[t - at].data_ptr())
+            decode_step_tensors(c, dec[0][t], dec[1][t], dec[2][t], dec[3][t], chained=True)
+        lib.akv_debug_set_decode_trace(None)
+        torch.cuda.synchronize()
+        trs = [b.view(-1, 16).cpu().numpy().astype(np.float64) for b in bufs]
     t0 = min(tr[tr[:, 0] > 0, 0].min() for tr in trs)
     print(f"{name} T={T}: us relative to the first traced CTA start; med / p90 / max over CTAs")
     print("step  ctas  start(min,med,max)      plan_done(med)  first_page(med,max)  last_page(med,max)  end(med,p90,max)")
