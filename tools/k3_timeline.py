@@ -82,6 +82,12 @@ def main():
         if prev_end is not None:
             print(f"      step start (min) - previous step end (max): {r[:,0].min() - prev_end:6.1f} us;"
                   f" first page (max) - previous end (max): {fp.max() - prev_end:6.1f}")
+        # the CTA that ends last: its stamps (0 start, 1 planned, 2 first page, 3 last page,
+        # 8 publish start, 9 partial released, 10 segment done, 4 epilogue warps done)
+        k = int(np.argmax(end))
+        names = {0: "start", 1: "plan", 2: "first", 3: "last", 8: "pub", 9: "rel", 10: "seg", 4: "epi"}
+        print("      last CTA:", ", ".join(f"{names[j]} {r[k, j]:.1f}" for j in (0, 1, 2, 3, 8, 9, 10, 4)
+                                         if tr[ok][k, j] > 0))
         prev_end = end.max()
 
 
