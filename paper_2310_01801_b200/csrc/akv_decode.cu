@@ -561,13 +561,15 @@ __device__ void policy_v3(const DecParams& p, const HeadCtx& hc, float lse, int*
 }
 
 // ---------------------------------------------------------------------------
-// Epilogue of one head (consumer warps only, named barrier 1).
+// Epilogue of one head: the combine of its split-K partials, its output and
+// live count, and (evicting heads) its policy - run by the group CS of the
+// head's last contributor.
 template <typename CS, int D, bool kPolicy = true>
 __device__ void head_epilogue(const DecParams& p, const HeadCtx& hc, int nparts, int rv,
                               int* hist, int* red_i) {
-  constexpr int NC = CS::kThreads, NW = CS::kWarps;
-  const int tid = CS::tid(), lane = tid & 31, warp = tid >> 5;
-  const int g = hc.g, L = hc.L, n = hc.n;
+  constexpr int NC = CS::kThreads;
+  const int tid = CS::tid();
+  const int g = hc.g, n = hc.n;
   // combine the partials of all contributing CTAs; every thread issues its
   // loads for a batch of parts (max, sum and its output dims) at once, so a
   // batch costs one L2 round trip
@@ -1538,9 +1540,12 @@ extern "C" int akv_decode_workspace_init(void* ws, size_t bytes, int32_t B, int3
 }
 
 static unsigned long long* trace_for(const akv_decode_args* a) {
-  if (!g_dec_trace || g_dec_trace_ring <= 1) return g_dec_trace;
+  if (!g_dec_trace) return nullptr;
   int sms = 0;
-  if (current_sm_count(&sms) != cudaSuccess) return g_dec_trace;
+  if (current_sm_count(&sms) != cudaSuccess) return nullptr;
+  // the trace buffers hold [2*SMs, 16] stamps: a larger grid (AKV_K3_GRID) is not traced
+  if (k3_grid(sms) > 2 * sms) return nullptr;
+  if (g_dec_trace_ring <= 1) return g_dec_trace;
   const int slot = (a->pos - a->prompt_len) % g_dec_trace_ring;
   return g_dec_trace + (size_t)slot * 2 * sms * 16;
 }
