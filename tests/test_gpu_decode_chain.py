@@ -164,3 +164,41 @@ def test_decode_steps_call_matches_step_by_step(B, H, N, D, d, dtype):
     assert a[4] == b[4] == N + D
     for x, y in zip(a[3], b[3]):
         np.testing.assert_array_equal(x, y)
+
+
+def test_decode_steps_chunk_edges():
+    """decode_steps_tensors with 1-step and 0-step calls between longer ones
+    equals one decode_step_tensors call per step (outputs, live counts)."""
+    from paper_2310_01801_b200 import decode_steps_tensors
+
+    w = _workload(2, 6, 200, 12, 128, seed=77)
+    qd, kd, vd, cd = _inputs(w)
+    dev = qd.device
+    sl = torch.tensor(w.slopes, dtype=torch.float32, device=dev)
+    sk = torch.tensor(w.sinks, dtype=torch.float32, device=dev)
+    N, D = w.N, w.D
+    runs = []
+    for mode in ("steps", "single"):
+        res, c = encode_prompt_tensors(qd, kd, vd, cd, ProfilerConfig(recovery_threshold=0.98),
+                                       prompt_len=N, max_new_tokens=D, slopes=sl, sinks=sk)
+        outs = torch.zeros(D, 2, w.H, 128, dtype=torch.float32, device=dev)
+        if mode == "steps":
+            cls = cd[:, N:].t().contiguous()
+            t0 = 0
+            for n in (1, 0, 5, 1, 0, 5):
+                sl_ = slice(N + t0, N + t0 + n)
+                ret = decode_steps_tensors(c, qd[:, :, sl_], kd[:, :, sl_], vd[:, :, sl_],
+                                           cls[t0:t0 + n], out=outs[t0:t0 + n], chained=True)
+                assert ret.shape[0] == n
+                t0 += n
+            assert t0 == D
+        else:
+            for t in range(D):
+                decode_step_tensors(c, qd[:, :, N + t], kd[:, :, N + t], vd[:, :, N + t],
+                                    cd[:, N + t].contiguous(), out=outs[t], chained=True)
+        torch.cuda.synchronize()
+        c.check()
+        runs.append((outs.cpu().numpy(), c.live.cpu().numpy(), c.seq_len))
+    np.testing.assert_array_equal(runs[0][0], runs[1][0])
+    np.testing.assert_array_equal(runs[0][1], runs[1][1])
+    assert runs[0][2] == runs[1][2] == N + D
