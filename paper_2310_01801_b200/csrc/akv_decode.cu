@@ -110,6 +110,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
     if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 16 + (slot)] = gtimer(); \
   } while (0)
 
+// FREQUENT-policy phase stamps (cycles) into trace slots 11-15, debug builds
+// only (-DAKV_TRACE_EPI; tools/k3_regimes.py reports them): policy start,
+// pass A done, decision made, action done, evictions done
+#ifdef AKV_TRACE_EPI
+#define AKV_EPI_STAMP(slot)                                                            \
+  do {                                                                                 \
+    if (p.trace && freq && tid == 0) p.trace[blockIdx.x * 16 + (slot)] = clock64();    \
+  } while (0)
+#else
+#define AKV_EPI_STAMP(slot) do {} while (0)
+#endif
+
 // owner CTA of flattened page pg when P pages are split evenly over `grid`
 // (CTA i owns [floor(i*P/grid), floor((i+1)*P/grid)))
 __device__ __forceinline__ int page_owner(long long pg, long long P, int grid) {
@@ -272,6 +284,7 @@ __device__ void policy_v3(const DecParams& p, const HeadCtx& hc, float lse, int*
     return ka > kb || (ka == kb && pa < pb);
   };
 
+  AKV_EPI_STAMP(11);
   // ---------------- pass A ----------------
   unsigned long long minF_k = ~0ull, maxN_k = 0ull;
   int minF_p = -1, maxN_p = 0x7fffffff, maxN_slot = -1, maxN_ck = 0, anyN = 0, cntF = 0;
@@ -311,6 +324,7 @@ __device__ void policy_v3(const DecParams& p, const HeadCtx& hc, float lse, int*
       }
     }
   }
+  AKV_EPI_STAMP(12);
   // group reductions
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -397,6 +411,7 @@ __device__ void policy_v3(const DecParams& p, const HeadCtx& hc, float lse, int*
   }
   CS::sync();
   int mode = s_mode;
+  AKV_EPI_STAMP(13);
   if (freq) {
     if (mode == 0) {
       if (tid == 0 && s_add >= 0) meta[s_add] = __ldcg(meta + s_add) | kInF;
@@ -473,6 +488,7 @@ __device__ void policy_v3(const DecParams& p, const HeadCtx& hc, float lse, int*
     }
     CS::sync();
   }
+  AKV_EPI_STAMP(14);
   uint4* kw = static_cast<uint4*>(p.kc) + hc.base * rv;
   uint4* vw = static_cast<uint4*>(p.vc) + hc.base * rv;
   int n_keep;
@@ -553,6 +569,7 @@ __device__ void policy_v3(const DecParams& p, const HeadCtx& hc, float lse, int*
     }
   }
   if (tid == 0) {
+    AKV_EPI_STAMP(15);
     p.live_out[g] = n_keep;
     if (p.evicted) p.evicted[g] = n - n_keep;
     p.counter[g] = 0;

@@ -83,8 +83,8 @@ def regime(name, T, reps=3):
             "frequent_epilogues": int(tr[ok, 6].sum()), "radix_fallbacks": int(tr[ok, 7].sum()),
             "isolated_step_us": float(rel[:, 4].max()),
             "plan_us_median": float(np.median(rel[:, 1] - rel[:, 0])),
-            # slots 11-15: plan phase (-DAKV_TRACE_PLAN) or FREQUENT epilogue phase
-            # (-DAKV_TRACE_EPI) cycle stamps, relative to slot 11
+            # slots 11-15: FREQUENT policy phase cycle stamps of a -DAKV_TRACE_EPI
+            # build (pass A, decision, action, evictions), relative to slot 11
             "phase_cycles_median": [float(np.median((tr[:, j] - tr[:, 11])[(tr[:, 11] > 0) & (tr[:, j] > 0)]))
                                     if ((tr[:, 11] > 0) & (tr[:, j] > 0)).any() else None
                                     for j in (12, 13, 14, 15)],
